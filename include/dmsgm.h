@@ -1,0 +1,142 @@
+/*
+ * dmsgm.h -- C ABI of the B200 (sm_100a) grid-block Dual-Mode SGM motion-masking step.
+ *
+ * Method: Henderson & Vertescher, "An Analysis of Parallelized Motion Masking Using
+ * Dual-Mode Single Gaussian Models" (arXiv 1702.05156), implementing Yi et al.'s
+ * DMSGM.  Per frame and per N x N grid block G_i (Eq. 4 kept general, |G_i| = N^2):
+ *   (1) warp + mix the previous models through the frame's homography into the
+ *       "previous values after motion compensation" mu~, sigma~, alpha~ (§2.2 P:89,
+ *       §2.4; readings R2-R7), with age decay (R7);
+ *   (2) block mean M_i (Eq. 4);
+ *   (3) dual-mode update: match tests Eqs. 8-9, mean/variance/age updates
+ *       Eqs. 3, 5, 6, 7, candidate reset, swap Eq. 10;
+ *   (4) per-pixel mask (App. E, variance reading R14).
+ * DESIGN.md §2 lists every reading; §3 the HBM layout.
+ *
+ * Conventions
+ *  - All calls return an int status (DMSGM_OK or a negative DMSGM_E* code).  On error
+ *    a message is available from dmsgm_last_error(ctx) (or dmsgm_last_error(NULL) for
+ *    dmsgm_create failures).  Argument errors are detected synchronously and enqueue
+ *    nothing.  Asynchronous device faults surface as DMSGM_ECUDA at a later call.
+ *  - Unless stated otherwise every buffer pointer is a DEVICE pointer on the context's
+ *    device, owned by the caller; the library never frees or retains them.  The
+ *    context owns its model state (two ping-pong buffers of 6 fp32 planes per stream),
+ *    per-stream "fresh" flags, any captured CUDA graph and the staging buffers of
+ *    dmsgm_step_host.
+ *  - A context is not thread-safe; use one context per device and host thread.
+ *  - Images are 8-bit grayscale, row-major, `width` pixels per row with a row pitch
+ *    in bytes.  Pitches must be multiples of 16 and >= width; frame/mask base pointers
+ *    must be 16-byte aligned; homography pointers 8-byte aligned.
+ *  - Streams: `num_streams` (S) independent video streams are processed per call;
+ *    stream s of a batch lives at byte offset s*height*pitch.
+ */
+#ifndef DMSGM_H
+#define DMSGM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DMSGM_OK       0
+#define DMSGM_EINVAL  -1 /* null pointer, width%block or height%block != 0, width%4 != 0,
+                            block not in {1,2,4,8,16}, bad params, misaligned pointer/pitch,
+                            invalid state values in dmsgm_set_state                      */
+#define DMSGM_ENOMEM  -2 /* device or host allocation failed                             */
+#define DMSGM_ECUDA   -3 /* CUDA runtime error (no device, launch failure, async fault)   */
+#define DMSGM_ESTATE  -4 /* stream index out of range                                    */
+
+/* Parameters of the method (all explicit; there are no hidden defaults in the kernel). */
+typedef struct {
+    float theta_s;            /* match gate of Eqs. 8-9; paper gives no value, 4 (R15) */
+    float theta_d;            /* classification gate THETA_D of App. E P:657 (R14); 4 (R15)          */
+    float var_init;           /* variance of a reset / new model, 255 (App. E)          */
+    float age_cap;            /* age cap, 30 (App. E AGE_THRESH P:616)                         */
+    float var_floor_match;    /* variance floor in the match test, 0.1 (App. E)         */
+    float var_floor_classify; /* variance floor in classification, 0.25 (App. E)               */
+    float decay_lambda;       /* age-decay rate lambda (R7); 0 disables the decay bitwise             */
+    float decay_var_thresh;   /* age-decay variance threshold theta_v (R7)                           */
+    int   num_streams;        /* S >= 1: independent streams batched per call                         */
+    int   update_rule;        /* 0: Eqs. 3/5/7 (R10); 1: App. E code rule alpha = 1/age (R27)         */
+    int   classify_rule;      /* 0: theta_d*max(var_A, f_c) (R14); 1: App. E theta_d*max(f_c, I) (R28) */
+} dmsgm_params;
+
+typedef struct dmsgm_ctx dmsgm_ctx;
+
+/* Static facts about a context (for the harness: bytes, launch counts). */
+typedef struct {
+    int width, height, block;      /* W, H, N                                   */
+    int blocks_x, blocks_y;        /* Wb = W/N, Hb = H/N                        */
+    int num_streams;               /* S                                         */
+    int kernels_per_step;          /* kernel launches per dmsgm_step (1)       */
+    size_t state_bytes;            /* one state buffer: S*6*Hb*Wb*4            */
+    double algorithmic_bytes_per_frame; /* frame read + mask write + state read+write, one stream */
+} dmsgm_info;
+
+/* Create a context on CUDA device `device` (W, H in pixels, N = block).  Allocates two
+ * state buffers (S*6*Hb*Wb fp32 each) and the fresh flags; all streams start "fresh"
+ * (their first step initialises A = C = (M, var_init, 1), R8).  No kernel is launched. */
+int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int device,
+                 dmsgm_ctx** out);
+
+/* One frame for all S streams.  frames: u8 [S][height][frame_pitch] (device);
+ * homographies: f64 [S][9] (device), row-major, mapping frame-t continuous pixel
+ * coordinates to frame-(t-1) coordinates (R3), ignored for streams on their first
+ * frame but always read; masks: u8 [S][height][mask_pitch] (device), written with
+ * {0,255}.  Enqueued on `cuda_stream` (a cudaStream_t, NULL = legacy default stream);
+ * returns after the enqueue (asynchronous).  Exactly one kernel launch. */
+int dmsgm_step(dmsgm_ctx* ctx, const uint8_t* frames, size_t frame_pitch,
+               const double* homographies, uint8_t* masks, size_t mask_pitch, void* cuda_stream);
+
+/* T consecutive frames per stream: frames u8 [T][S][height][frame_pitch], homographies
+ * f64 [T][S][9], masks u8 [T][S][height][mask_pitch] (device).  The T launches are
+ * captured once into a CUDA graph (re-captured when T or a pointer/pitch changes) and
+ * replayed on `cuda_stream`.  Asynchronous. */
+int dmsgm_step_n(dmsgm_ctx* ctx, int T, const uint8_t* frames, size_t frame_pitch,
+                 const double* homographies, uint8_t* masks, size_t mask_pitch, void* cuda_stream);
+
+/* End-to-end step from HOST memory: frames u8 [S][height][frame_pitch] and homographies
+ * f64 [S][9] in host memory (pinned for full speed), masks u8 [S][height][mask_pitch]
+ * written to host memory.  Streams are split into chunks whose H2D copy, kernel and
+ * D2H copy are pipelined over internal CUDA streams ordered after `cuda_stream`.
+ * SYNCHRONOUS: returns when the masks are in host memory.  Device staging buffers are
+ * allocated on the first call and kept until dmsgm_destroy. */
+int dmsgm_step_host(dmsgm_ctx* ctx, const uint8_t* host_frames, size_t frame_pitch,
+                    const double* host_homographies, uint8_t* host_masks, size_t mask_pitch,
+                    void* cuda_stream);
+
+/* Mark stream `stream` (or all, -1) fresh: its next step re-initialises (R8).
+ * Synchronises the device first. */
+int dmsgm_reset(dmsgm_ctx* ctx, int stream);
+
+/* Copy stream `stream`'s current models to HOST memory: f32 [6][Hb][Wb], planes
+ * mu_A, var_A, age_A, mu_C, var_C, age_C.  Synchronises the device first. */
+int dmsgm_get_state(dmsgm_ctx* ctx, int stream, float* host_out);
+
+/* Load stream `stream`'s models from HOST memory (same layout) and mark it initialised.
+ * Values must be finite with 0 <= mu <= 255, var >= 0, 0 <= age <= age_cap (else
+ * DMSGM_EINVAL, nothing written).  Synchronises the device first. */
+int dmsgm_set_state(dmsgm_ctx* ctx, int stream, const float* host_in);
+
+/* 1 if stream `stream` has been initialised (stepped at least once or set), else 0;
+ * negative on error.  Synchronises the device first. */
+int dmsgm_is_initialised(dmsgm_ctx* ctx, int stream);
+
+int dmsgm_get_info(const dmsgm_ctx* ctx, dmsgm_info* out);
+
+/* Last error message of `ctx` ("" if none); with ctx == NULL, the last create error of
+ * the calling thread.  The string lives until the next call on the same context. */
+const char* dmsgm_last_error(const dmsgm_ctx* ctx);
+
+/* Free all device/host resources of the context (synchronises the device). */
+void dmsgm_destroy(dmsgm_ctx* ctx);
+
+/* Library version string, e.g. "dmsgm-b200 0.1 sm_100a". */
+const char* dmsgm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DMSGM_H */

@@ -1,0 +1,427 @@
+// dmsgm.cu -- host side of the C ABI declared in include/dmsgm.h.
+//
+// Owns the device-resident model state (two ping-pong buffers, SoA, fp32,
+// [S][6][Hb][Wb]) and per-stream fresh flags (two ping-pong arrays [S]); launches
+// the fused step kernel (dmsgm_kernel.cuh) once per frame batch; captures T-step
+// batches into CUDA graphs; pipelines host<->device copies for dmsgm_step_host.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <new>
+
+#include "dmsgm.h"
+#include "dmsgm_kernel.cuh"
+
+using namespace dmsgm;
+
+namespace {
+
+constexpr int kPipeStreams = 3;
+
+struct GraphSlot {
+    bool valid = false;
+    int T = 0, parity = 0;
+    const void* frames = nullptr;
+    const void* H = nullptr;
+    const void* masks = nullptr;
+    size_t fpitch = 0, mpitch = 0;
+    cudaGraphExec_t exec = nullptr;
+};
+
+thread_local char g_create_err[512] = "";
+
+}  // namespace
+
+struct dmsgm_ctx {
+    int W, H, N, Wb, Hb, S, device;
+    dmsgm_params p;
+    float* state[2];
+    uint8_t* fresh[2];
+    int cur;
+    cudaStream_t capture_stream;
+    GraphSlot graphs[2];
+    int graph_next;
+    // dmsgm_step_host staging
+    uint8_t* st_frames;
+    uint8_t* st_masks;
+    double* st_H;
+    cudaStream_t pipe[kPipeStreams];
+    cudaEvent_t ev_start;
+    bool pipe_ready;
+    char err[512];
+};
+
+namespace {
+
+int fail(dmsgm_ctx* c, int code, const char* fmt, ...) {
+    char* buf = c ? c->err : g_create_err;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, 512, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_fail(dmsgm_ctx* c, cudaError_t e, const char* what) {
+    return fail(c, DMSGM_ECUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+// Scoped device switch (restores the caller's current device).
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() {
+        int now;
+        if (prev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != prev) cudaSetDevice(prev);
+    }
+};
+
+bool params_ok(const dmsgm_params* p, char* why, size_t n) {
+    if (!p) { snprintf(why, n, "params is NULL"); return false; }
+    if (!(p->theta_s > 0.f) || !(p->theta_d > 0.f)) { snprintf(why, n, "theta_s, theta_d must be > 0"); return false; }
+    if (!(p->age_cap >= 1.f) || !isfinite(p->age_cap)) { snprintf(why, n, "age_cap must be >= 1"); return false; }
+    if (!(p->var_init >= 0.f) || !isfinite(p->var_init)) { snprintf(why, n, "var_init must be >= 0"); return false; }
+    if (!(p->var_floor_match > 0.f) || !(p->var_floor_classify > 0.f)) { snprintf(why, n, "variance floors must be > 0"); return false; }
+    if (!(p->decay_lambda >= 0.f) || !(p->decay_var_thresh >= 0.f)) { snprintf(why, n, "decay params must be >= 0"); return false; }
+    if (p->num_streams < 1 || p->num_streams > 65535) { snprintf(why, n, "num_streams must be in [1, 65535]"); return false; }
+    if (p->update_rule < 0 || p->update_rule > 1) { snprintf(why, n, "update_rule must be 0 or 1"); return false; }
+    if (p->classify_rule < 0 || p->classify_rule > 1) { snprintf(why, n, "classify_rule must be 0 or 1"); return false; }
+    return true;
+}
+
+KParams kparams(const dmsgm_params& p) {
+    KParams k;
+    k.theta_s = p.theta_s; k.theta_d = p.theta_d; k.var_init = p.var_init; k.age_cap = p.age_cap;
+    k.f_m = p.var_floor_match; k.f_c = p.var_floor_classify;
+    k.lambda = p.decay_lambda; k.theta_v = p.decay_var_thresh;
+    k.update_rule = p.update_rule; k.classify_rule = p.classify_rule;
+    return k;
+}
+
+size_t plane_elems(const dmsgm_ctx* c) { return (size_t)c->Wb * (size_t)c->Hb; }
+
+int strips_of(const dmsgm_ctx* c) {
+    switch (c->N) {
+        case 1: return c->Wb / Geom<1>::BPT;
+        case 2: return c->Wb / Geom<2>::BPT;
+        default: return c->Wb;
+    }
+}
+
+// Enqueue one kernel for streams [s0, s0+count) of the batch.
+cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, const double* H,
+                        uint8_t* masks, size_t mpitch, int s0, int count, int parity,
+                        cudaStream_t stream) {
+    StepArgs a;
+    a.frames = frames;
+    a.fstride = (long long)c->H * (long long)fpitch;
+    a.fpitch = (long long)fpitch;
+    a.H = H;
+    a.masks = masks;
+    a.mstride = (long long)c->H * (long long)mpitch;
+    a.mpitch = (long long)mpitch;
+    const size_t sstride = 6 * plane_elems(c);
+    a.prev = c->state[parity] + (size_t)s0 * sstride;
+    a.next = c->state[parity ^ 1] + (size_t)s0 * sstride;
+    a.fresh_in = c->fresh[parity] + s0;
+    a.fresh_out = c->fresh[parity ^ 1] + s0;
+    a.Wb = c->Wb;
+    a.Hb = c->Hb;
+    a.Wstrips = strips_of(c);
+    a.plane = (long long)plane_elems(c);
+    a.kp = kparams(c->p);
+    dim3 block(kCtaX, kCtaY, 1);
+    dim3 grid((a.Wstrips + kCtaX - 1) / kCtaX, (c->Hb + kCtaY - 1) / kCtaY, count);
+    switch (c->N) {
+        case 1: dmsgm_step_kernel<1><<<grid, block, 0, stream>>>(a); break;
+        case 2: dmsgm_step_kernel<2><<<grid, block, 0, stream>>>(a); break;
+        case 4: dmsgm_step_kernel<4><<<grid, block, 0, stream>>>(a); break;
+        case 8: dmsgm_step_kernel<8><<<grid, block, 0, stream>>>(a); break;
+        case 16: dmsgm_step_kernel<16><<<grid, block, 0, stream>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+int check_images(dmsgm_ctx* c, const void* frames, size_t fpitch, const void* H, const void* masks,
+                 size_t mpitch) {
+    if (!frames || !H || !masks) return fail(c, DMSGM_EINVAL, "null frames/homographies/masks pointer");
+    if (((uintptr_t)frames & 15) || ((uintptr_t)masks & 15))
+        return fail(c, DMSGM_EINVAL, "frames and masks must be 16-byte aligned");
+    if ((uintptr_t)H & 7) return fail(c, DMSGM_EINVAL, "homographies must be 8-byte aligned");
+    if (fpitch < (size_t)c->W || (fpitch & 15)) return fail(c, DMSGM_EINVAL, "frame_pitch must be >= width and a multiple of 16");
+    if (mpitch < (size_t)c->W || (mpitch & 15)) return fail(c, DMSGM_EINVAL, "mask_pitch must be >= width and a multiple of 16");
+    return DMSGM_OK;
+}
+
+void destroy_graphs(dmsgm_ctx* c) {
+    for (auto& g : c->graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g = GraphSlot();
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dmsgm_version(void) { return "dmsgm-b200 0.1 sm_100a"; }
+
+int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int device, dmsgm_ctx** out) {
+    g_create_err[0] = 0;
+    if (!out) return fail(nullptr, DMSGM_EINVAL, "out is NULL");
+    *out = nullptr;
+    char why[256];
+    if (!params_ok(p, why, sizeof why)) return fail(nullptr, DMSGM_EINVAL, "%s", why);
+    if (block != 1 && block != 2 && block != 4 && block != 8 && block != 16)
+        return fail(nullptr, DMSGM_EINVAL, "block must be 1, 2, 4, 8 or 16 (got %d)", block);
+    if (width <= 0 || height <= 0 || width % block || height % block)
+        return fail(nullptr, DMSGM_EINVAL, "width/height must be positive multiples of block (R1)");
+    if (width % 4) return fail(nullptr, DMSGM_EINVAL, "width must be a multiple of 4");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return fail(nullptr, DMSGM_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(nullptr, DMSGM_EINVAL, "device %d out of range (%d devices)", device, ndev);
+    DeviceGuard g(device);
+    if (!g.ok) return fail(nullptr, DMSGM_ECUDA, "cudaSetDevice(%d) failed", device);
+
+    dmsgm_ctx* c = new (std::nothrow) dmsgm_ctx();
+    if (!c) return fail(nullptr, DMSGM_ENOMEM, "host allocation failed");
+    c->W = width; c->H = height; c->N = block;
+    c->Wb = width / block; c->Hb = height / block;
+    c->S = p->num_streams; c->device = device; c->p = *p;
+    const size_t sbytes = (size_t)c->S * 6 * plane_elems(c) * sizeof(float);
+    for (int i = 0; i < 2; ++i) {
+        if ((e = cudaMalloc(&c->state[i], sbytes)) != cudaSuccess ||
+            (e = cudaMalloc(&c->fresh[i], (size_t)c->S)) != cudaSuccess) {
+            dmsgm_destroy(c);
+            return fail(nullptr, DMSGM_ENOMEM, "cudaMalloc of %zu B failed: %s", sbytes, cudaGetErrorString(e));
+        }
+    }
+    if ((e = cudaMemset(c->state[0], 0, sbytes)) != cudaSuccess ||
+        (e = cudaMemset(c->state[1], 0, sbytes)) != cudaSuccess ||
+        (e = cudaMemset(c->fresh[0], 1, (size_t)c->S)) != cudaSuccess ||
+        (e = cudaMemset(c->fresh[1], 1, (size_t)c->S)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaDeviceSynchronize()) != cudaSuccess) {
+        dmsgm_destroy(c);
+        return fail(nullptr, DMSGM_ECUDA, "context init: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return DMSGM_OK;
+}
+
+int dmsgm_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, const double* H, uint8_t* masks,
+               size_t mpitch, void* cuda_stream) {
+    if (!c) return DMSGM_EINVAL;
+    int rc = check_images(c, frames, fpitch, H, masks, mpitch);
+    if (rc) return rc;
+    DeviceGuard g(c->device);
+    if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
+    cudaError_t e = launch_step(c, frames, fpitch, H, masks, mpitch, 0, c->S, c->cur,
+                                (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_step launch");
+    c->cur ^= 1;
+    return DMSGM_OK;
+}
+
+int dmsgm_step_n(dmsgm_ctx* c, int T, const uint8_t* frames, size_t fpitch, const double* H,
+                 uint8_t* masks, size_t mpitch, void* cuda_stream) {
+    if (!c) return DMSGM_EINVAL;
+    if (T < 1) return fail(c, DMSGM_EINVAL, "T must be >= 1");
+    int rc = check_images(c, frames, fpitch, H, masks, mpitch);
+    if (rc) return rc;
+    DeviceGuard g(c->device);
+    if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
+    const size_t fframe = (size_t)c->S * c->H * fpitch, mframe = (size_t)c->S * c->H * mpitch;
+    GraphSlot* slot = nullptr;
+    for (auto& gs : c->graphs)
+        if (gs.valid && gs.T == T && gs.parity == c->cur && gs.frames == frames && gs.H == H &&
+            gs.masks == masks && gs.fpitch == fpitch && gs.mpitch == mpitch)
+            slot = &gs;
+    cudaError_t e;
+    if (!slot) {
+        slot = &c->graphs[c->graph_next];
+        c->graph_next ^= 1;
+        if (slot->exec) cudaGraphExecDestroy(slot->exec);
+        *slot = GraphSlot();
+        cudaGraph_t graph;
+        e = cudaStreamBeginCapture(c->capture_stream, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamBeginCapture");
+        int parity = c->cur;
+        cudaError_t le = cudaSuccess;
+        for (int t = 0; t < T && le == cudaSuccess; ++t) {
+            le = launch_step(c, frames + t * fframe, fpitch, H + (size_t)t * c->S * 9, masks + t * mframe,
+                             mpitch, 0, c->S, parity, c->capture_stream);
+            parity ^= 1;
+        }
+        e = cudaStreamEndCapture(c->capture_stream, &graph);
+        if (le != cudaSuccess) return cuda_fail(c, le, "dmsgm_step_n capture launch");
+        if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamEndCapture");
+        e = cudaGraphInstantiate(&slot->exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
+        slot->valid = true; slot->T = T; slot->parity = c->cur;
+        slot->frames = frames; slot->H = H; slot->masks = masks;
+        slot->fpitch = fpitch; slot->mpitch = mpitch;
+    }
+    e = cudaGraphLaunch(slot->exec, (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphLaunch");
+    if (T & 1) c->cur ^= 1;
+    return DMSGM_OK;
+}
+
+int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double* hH, uint8_t* hm,
+                    size_t mpitch, void* cuda_stream) {
+    if (!c) return DMSGM_EINVAL;
+    if (!hf || !hH || !hm) return fail(c, DMSGM_EINVAL, "null host pointer");
+    if (fpitch < (size_t)c->W || mpitch < (size_t)c->W)
+        return fail(c, DMSGM_EINVAL, "pitches must be >= width");
+    DeviceGuard g(c->device);
+    if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
+    cudaError_t e;
+    const size_t dpitch = ((size_t)c->W + 15) & ~(size_t)15;
+    const size_t fimg = (size_t)c->H * dpitch;
+    if (!c->pipe_ready) {
+        const size_t nb = (size_t)c->S * fimg;
+        if ((e = cudaMalloc(&c->st_frames, nb)) != cudaSuccess || (e = cudaMalloc(&c->st_masks, nb)) != cudaSuccess ||
+            (e = cudaMalloc(&c->st_H, (size_t)c->S * 9 * sizeof(double))) != cudaSuccess)
+            return fail(c, DMSGM_ENOMEM, "staging cudaMalloc failed: %s", cudaGetErrorString(e));
+        for (int i = 0; i < kPipeStreams; ++i)
+            if ((e = cudaStreamCreateWithFlags(&c->pipe[i], cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_fail(c, e, "cudaStreamCreate");
+        if ((e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(c, e, "cudaEventCreate");
+        c->pipe_ready = true;
+    }
+    if ((e = cudaEventRecord(c->ev_start, (cudaStream_t)cuda_stream)) != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
+    for (int i = 0; i < kPipeStreams; ++i)
+        if ((e = cudaStreamWaitEvent(c->pipe[i], c->ev_start, 0)) != cudaSuccess) return cuda_fail(c, e, "cudaStreamWaitEvent");
+    // chunks of streams: H2D(k) || kernel(k-1) || D2H(k-2) across the pipe streams
+    const int nchunks = c->S < 8 ? c->S : 8;
+    const int per = (c->S + nchunks - 1) / nchunks;
+    const int parity = c->cur;
+    for (int s0 = 0, k = 0; s0 < c->S; s0 += per, ++k) {
+        const int cnt = (c->S - s0) < per ? (c->S - s0) : per;
+        cudaStream_t st = c->pipe[k % kPipeStreams];
+        uint8_t* df = c->st_frames + (size_t)s0 * fimg;
+        uint8_t* dm = c->st_masks + (size_t)s0 * fimg;
+        if ((e = cudaMemcpy2DAsync(df, dpitch, hf + (size_t)s0 * c->H * fpitch, fpitch, c->W, (size_t)cnt * c->H,
+                                   cudaMemcpyHostToDevice, st)) != cudaSuccess)
+            return cuda_fail(c, e, "H2D frames");
+        if ((e = cudaMemcpyAsync(c->st_H + (size_t)s0 * 9, hH + (size_t)s0 * 9, (size_t)cnt * 9 * sizeof(double),
+                                 cudaMemcpyHostToDevice, st)) != cudaSuccess)
+            return cuda_fail(c, e, "H2D homographies");
+        if ((e = launch_step(c, df, dpitch, c->st_H + (size_t)s0 * 9, dm, dpitch, s0, cnt, parity, st)) != cudaSuccess)
+            return cuda_fail(c, e, "dmsgm_step_host launch");
+        if ((e = cudaMemcpy2DAsync(hm + (size_t)s0 * c->H * mpitch, mpitch, dm, dpitch, c->W, (size_t)cnt * c->H,
+                                   cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+            return cuda_fail(c, e, "D2H masks");
+    }
+    for (int i = 0; i < kPipeStreams; ++i)
+        if ((e = cudaStreamSynchronize(c->pipe[i])) != cudaSuccess) return cuda_fail(c, e, "dmsgm_step_host sync");
+    c->cur ^= 1;
+    return DMSGM_OK;
+}
+
+int dmsgm_reset(dmsgm_ctx* c, int stream) {
+    if (!c) return DMSGM_EINVAL;
+    if (stream < -1 || stream >= c->S) return fail(c, DMSGM_ESTATE, "stream %d out of range", stream);
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_reset sync");
+    if (stream == -1) e = cudaMemset(c->fresh[c->cur], 1, (size_t)c->S);
+    else e = cudaMemset(c->fresh[c->cur] + stream, 1, 1);
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_reset memset");
+    return DMSGM_OK;
+}
+
+int dmsgm_get_state(dmsgm_ctx* c, int stream, float* out) {
+    if (!c || !out) return c ? fail(c, DMSGM_EINVAL, "null output") : DMSGM_EINVAL;
+    if (stream < 0 || stream >= c->S) return fail(c, DMSGM_ESTATE, "stream %d out of range", stream);
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_get_state sync");
+    const size_t n = 6 * plane_elems(c);
+    e = cudaMemcpy(out, c->state[c->cur] + (size_t)stream * n, n * sizeof(float), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_get_state copy");
+    return DMSGM_OK;
+}
+
+int dmsgm_set_state(dmsgm_ctx* c, int stream, const float* in) {
+    if (!c || !in) return c ? fail(c, DMSGM_EINVAL, "null input") : DMSGM_EINVAL;
+    if (stream < 0 || stream >= c->S) return fail(c, DMSGM_ESTATE, "stream %d out of range", stream);
+    const size_t pe = plane_elems(c);
+    for (int m = 0; m < 2; ++m) {
+        const float* mu = in + (size_t)(3 * m) * pe;
+        const float* var = mu + pe;
+        const float* age = var + pe;
+        for (size_t i = 0; i < pe; ++i) {
+            if (!(mu[i] >= 0.f && mu[i] <= 255.f) || !(var[i] >= 0.f && isfinite(var[i])) ||
+                !(age[i] >= 0.f && age[i] <= c->p.age_cap))
+                return fail(c, DMSGM_EINVAL, "invalid state value at model %d index %zu", m, i);
+        }
+    }
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_set_state sync");
+    e = cudaMemcpy(c->state[c->cur] + (size_t)stream * 6 * pe, in, 6 * pe * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(c->fresh[c->cur] + stream, 0, 1);
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_set_state copy");
+    return DMSGM_OK;
+}
+
+int dmsgm_is_initialised(dmsgm_ctx* c, int stream) {
+    if (!c) return DMSGM_EINVAL;
+    if (stream < 0 || stream >= c->S) return fail(c, DMSGM_ESTATE, "stream %d out of range", stream);
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "sync");
+    uint8_t f = 1;
+    e = cudaMemcpy(&f, c->fresh[c->cur] + stream, 1, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e, "copy");
+    return f ? 0 : 1;
+}
+
+int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
+    if (!c || !out) return DMSGM_EINVAL;
+    out->width = c->W; out->height = c->H; out->block = c->N;
+    out->blocks_x = c->Wb; out->blocks_y = c->Hb; out->num_streams = c->S;
+    out->kernels_per_step = 1;
+    out->state_bytes = (size_t)c->S * 6 * plane_elems(c) * sizeof(float);
+    // frame read (1 B/px) + mask write (1 B/px) + state read + write (2 x 24 B per block)
+    out->algorithmic_bytes_per_frame = 2.0 * c->W * c->H + 2.0 * 24.0 * (double)plane_elems(c);
+    return DMSGM_OK;
+}
+
+const char* dmsgm_last_error(const dmsgm_ctx* c) { return c ? c->err : g_create_err; }
+
+void dmsgm_destroy(dmsgm_ctx* c) {
+    if (!c) return;
+    DeviceGuard g(c->device);
+    cudaDeviceSynchronize();
+    destroy_graphs(c);
+    for (int i = 0; i < 2; ++i) {
+        if (c->state[i]) cudaFree(c->state[i]);
+        if (c->fresh[i]) cudaFree(c->fresh[i]);
+    }
+    if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
+    if (c->pipe_ready) {
+        for (int i = 0; i < kPipeStreams; ++i) cudaStreamDestroy(c->pipe[i]);
+        cudaEventDestroy(c->ev_start);
+    }
+    if (c->st_frames) cudaFree(c->st_frames);
+    if (c->st_masks) cudaFree(c->st_masks);
+    if (c->st_H) cudaFree(c->st_H);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,206 @@
+"""Thin ctypes binding of include/dmsgm.h -- argument marshalling only.
+
+Every step of the path runs in libdmsgm.so (CUDA, sm_100a).  There is no CPU
+fallback: importing this module raises if the library is missing.  Tensors are
+PyTorch CUDA tensors used only as device memory; raw pointers and the current
+CUDA stream are handed to the C ABI unchanged.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, fields
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdmsgm.so")
+
+DMSGM_OK = 0
+DMSGM_EINVAL = -1
+DMSGM_ENOMEM = -2
+DMSGM_ECUDA = -3
+DMSGM_ESTATE = -4
+_ERRNAMES = {-1: "DMSGM_EINVAL", -2: "DMSGM_ENOMEM", -3: "DMSGM_ECUDA", -4: "DMSGM_ESTATE"}
+
+# Every symbol include/dmsgm.h declares (checked by tests/test_abi.py).
+EXPORTS = ("dmsgm_create", "dmsgm_step", "dmsgm_step_n", "dmsgm_step_host", "dmsgm_reset",
+           "dmsgm_get_state", "dmsgm_set_state", "dmsgm_is_initialised", "dmsgm_get_info",
+           "dmsgm_last_error", "dmsgm_destroy", "dmsgm_version")
+
+
+class DmsgmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class dmsgm_params(ctypes.Structure):
+    _fields_ = [("theta_s", ctypes.c_float), ("theta_d", ctypes.c_float),
+                ("var_init", ctypes.c_float), ("age_cap", ctypes.c_float),
+                ("var_floor_match", ctypes.c_float), ("var_floor_classify", ctypes.c_float),
+                ("decay_lambda", ctypes.c_float), ("decay_var_thresh", ctypes.c_float),
+                ("num_streams", ctypes.c_int), ("update_rule", ctypes.c_int),
+                ("classify_rule", ctypes.c_int)]
+
+
+class dmsgm_info(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int), ("height", ctypes.c_int), ("block", ctypes.c_int),
+                ("blocks_x", ctypes.c_int), ("blocks_y", ctypes.c_int),
+                ("num_streams", ctypes.c_int), ("kernels_per_step", ctypes.c_int),
+                ("state_bytes", ctypes.c_size_t), ("algorithmic_bytes_per_frame", ctypes.c_double)]
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -m paper_1702_05156_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P, i32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    lib.dmsgm_create.argtypes = [i32, i32, i32, ctypes.POINTER(dmsgm_params), i32, ctypes.POINTER(P)]
+    lib.dmsgm_step.argtypes = [P, P, sz, P, P, sz, P]
+    lib.dmsgm_step_n.argtypes = [P, i32, P, sz, P, P, sz, P]
+    lib.dmsgm_step_host.argtypes = [P, P, sz, P, P, sz, P]
+    lib.dmsgm_reset.argtypes = [P, i32]
+    lib.dmsgm_get_state.argtypes = [P, i32, P]
+    lib.dmsgm_set_state.argtypes = [P, i32, P]
+    lib.dmsgm_is_initialised.argtypes = [P, i32]
+    lib.dmsgm_get_info.argtypes = [P, ctypes.POINTER(dmsgm_info)]
+    lib.dmsgm_last_error.argtypes = [P]
+    lib.dmsgm_last_error.restype = ctypes.c_char_p
+    lib.dmsgm_destroy.argtypes = [P]
+    lib.dmsgm_destroy.restype = None
+    lib.dmsgm_version.argtypes = []
+    lib.dmsgm_version.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = load_library()
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+@dataclass
+class Params:
+    """dmsgm_params with the DESIGN.md defaults (R7, R15)."""
+    theta_s: float = 4.0
+    theta_d: float = 4.0
+    var_init: float = 255.0
+    age_cap: float = 30.0
+    var_floor_match: float = 0.1
+    var_floor_classify: float = 0.25
+    decay_lambda: float = 0.001
+    decay_var_thresh: float = 2500.0
+    num_streams: int = 1
+    update_rule: int = 0
+    classify_rule: int = 0
+
+    def to_c(self) -> dmsgm_params:
+        return dmsgm_params(*[getattr(self, f.name) for f in fields(self)])
+
+
+def _ptr(x) -> ctypes.c_void_p:
+    """Raw pointer of a torch tensor / numpy array / int (no copies)."""
+    if x is None:
+        return ctypes.c_void_p(0)
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    if isinstance(x, np.ndarray):
+        return ctypes.c_void_p(x.ctypes.data)
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _row_pitch(t) -> int:
+    """Row pitch in bytes of a [..., H, W] uint8 tensor/array (stride of dim -2)."""
+    if isinstance(t, np.ndarray):
+        return t.strides[-2]
+    return t.stride(-2) * t.element_size()
+
+
+class Dmsgm:
+    """Python view of one dmsgm_ctx.  Names follow include/dmsgm.h."""
+
+    def __init__(self, width: int, height: int, block: int, params: Params, device: int = 0):
+        self._lib = _lib
+        self.width, self.height, self.block = width, height, block
+        self.params = params
+        h = ctypes.c_void_p()
+        cp = params.to_c()
+        rc = self._lib.dmsgm_create(width, height, block, ctypes.byref(cp), device, ctypes.byref(h))
+        if rc != DMSGM_OK:
+            raise DmsgmError(rc, self._lib.dmsgm_last_error(None).decode())
+        self._h = h
+        self.info = self.get_info()
+
+    # -- helpers -------------------------------------------------------------
+    def _check(self, rc: int):
+        if rc < 0:
+            raise DmsgmError(rc, self._lib.dmsgm_last_error(self._h).decode())
+        return rc
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.dmsgm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- C ABI ---------------------------------------------------------------
+    def step(self, frames, homographies, masks, stream=None):
+        """frames/masks: uint8 CUDA [S][H][W] (row pitch from strides); homographies f64 [S][9]."""
+        self._check(self._lib.dmsgm_step(self._h, _ptr(frames), _row_pitch(frames), _ptr(homographies),
+                                         _ptr(masks), _row_pitch(masks), _stream_handle(stream)))
+
+    def step_n(self, T: int, frames, homographies, masks, stream=None):
+        """frames/masks: uint8 CUDA [T][S][H][W]; homographies f64 [T][S][9]."""
+        self._check(self._lib.dmsgm_step_n(self._h, T, _ptr(frames), _row_pitch(frames), _ptr(homographies),
+                                           _ptr(masks), _row_pitch(masks), _stream_handle(stream)))
+
+    def step_host(self, frames, homographies, masks, stream=None):
+        """HOST buffers (numpy or pinned CPU tensors); synchronous."""
+        self._check(self._lib.dmsgm_step_host(self._h, _ptr(frames), _row_pitch(frames), _ptr(homographies),
+                                              _ptr(masks), _row_pitch(masks), _stream_handle(stream)))
+
+    def reset(self, stream: int = -1):
+        self._check(self._lib.dmsgm_reset(self._h, stream))
+
+    def get_state(self, stream: int) -> np.ndarray:
+        out = np.empty((6, self.info.blocks_y, self.info.blocks_x), np.float32)
+        self._check(self._lib.dmsgm_get_state(self._h, stream, _ptr(out)))
+        return out
+
+    def set_state(self, stream: int, state: np.ndarray):
+        st = np.ascontiguousarray(state, np.float32)
+        assert st.shape == (6, self.info.blocks_y, self.info.blocks_x), st.shape
+        self._check(self._lib.dmsgm_set_state(self._h, stream, _ptr(st)))
+
+    def is_initialised(self, stream: int) -> bool:
+        return bool(self._check(self._lib.dmsgm_is_initialised(self._h, stream)))
+
+    def get_info(self) -> dmsgm_info:
+        info = dmsgm_info()
+        self._check(self._lib.dmsgm_get_info(self._h, ctypes.byref(info)))
+        return info
+
+
+def version() -> str:
+    return _lib.dmsgm_version().decode()

@@ -210,37 +210,121 @@ def homographies_for_stream(cfg: SeqConfig, s: int, T: Optional[int] = None,
 # ---------------------------------------------------------------------------
 # texture + objects
 # ---------------------------------------------------------------------------
-def _hash_u01(ix: np.ndarray, iy: np.ndarray, seed: int) -> np.ndarray:
-    """Counter-based hash of integer lattice coords -> [-1, 1)."""
-    m = np.uint64(0xFFFFFFFF)
-    h = (ix.astype(np.int64).astype(np.uint64) * np.uint64(0x9E3779B1)
-         + iy.astype(np.int64).astype(np.uint64) * np.uint64(0x85EBCA77)
-         + np.uint64(seed) * np.uint64(0xC2B2AE3D)) & m
-    h ^= h >> np.uint64(15)
-    h = (h * np.uint64(0x2C1B3C6D)) & m
-    h ^= h >> np.uint64(12)
-    h = (h * np.uint64(0x297A2D39)) & m
-    h ^= h >> np.uint64(15)
-    return (h.astype(np.float64) / 4294967296.0 * 2.0 - 1.0).astype(np.float32)
+class _NP:
+    """numpy backend (reference inputs for the parity tests)."""
+    name = "numpy"
+
+    def __init__(self):
+        self.f32 = np.float32
+
+    def grid(self, W, H):
+        xs = np.arange(W, dtype=np.float64) + 0.5
+        ys = np.arange(H, dtype=np.float64) + 0.5
+        return np.meshgrid(xs, ys)
+
+    def to_f32(self, a):
+        return a.astype(np.float32)
+
+    def i64(self, a):
+        return a.astype(np.int64)
+
+    sin = staticmethod(np.sin)
+    floor = staticmethod(np.floor)
+    abs = staticmethod(np.abs)
+
+    def clip(self, a, lo, hi):
+        return np.clip(a, lo, hi)
+
+    def zeros_u8(self, H, W):
+        return np.zeros((H, W), np.uint8)
+
+    def noise(self, seed_tuple, shape, sigma):
+        return np.random.default_rng(seed_tuple).normal(0.0, sigma, shape).astype(np.float32)
+
+    def to_u8(self, img):
+        return np.clip(np.rint(img), 0, 255).astype(np.uint8)
 
 
-def _texture(wx: np.ndarray, wy: np.ndarray, sp: _StreamParams) -> np.ndarray:
-    acc = np.zeros(wx.shape, np.float32)
+class _Torch:
+    """torch backend (fast bench inputs, e.g. on cuda); same recipe, different rounding/noise."""
+    name = "torch"
+
+    def __init__(self, device):
+        import torch
+        self.t = torch
+        self.device = torch.device(device)
+        self.f32 = torch.float32
+
+    def grid(self, W, H):
+        t = self.t
+        xs = t.arange(W, dtype=t.float64, device=self.device) + 0.5
+        ys = t.arange(H, dtype=t.float64, device=self.device) + 0.5
+        Y, X = t.meshgrid(ys, xs, indexing="ij")
+        return X, Y
+
+    def to_f32(self, a):
+        return a.to(self.t.float32)
+
+    def i64(self, a):
+        return a.to(self.t.int64)
+
+    def sin(self, a):
+        return self.t.sin(a)
+
+    def floor(self, a):
+        return self.t.floor(a)
+
+    def abs(self, a):
+        return self.t.abs(a)
+
+    def clip(self, a, lo, hi):
+        return self.t.clamp(a, lo, hi)
+
+    def zeros_u8(self, H, W):
+        return self.t.zeros((H, W), dtype=self.t.uint8, device=self.device)
+
+    def noise(self, seed_tuple, shape, sigma):
+        g = self.t.Generator(device=self.device)
+        g.manual_seed((int(seed_tuple[0]) * 1000003 + int(seed_tuple[1])) % (2**63 - 1))
+        return self.t.randn(shape, generator=g, device=self.device, dtype=self.t.float32) * sigma
+
+    def to_u8(self, img):
+        return self.t.clamp(self.t.round(img), 0, 255).to(self.t.uint8)
+
+
+_NUMPY = _NP()
+
+
+def _hash_u01(bk, ix, iy, seed: int):
+    """Counter-based hash of integer lattice coords -> [-1, 1) (identical low bits on both backends)."""
+    m = 0xFFFFFFFF
+    h = (ix * 0x9E3779B1 + iy * 0x85EBCA77 + (seed * 0xC2B2AE3D & m)) & m
+    h = h ^ (h >> 15)
+    h = (h * 0x2C1B3C6D) & m
+    h = h ^ (h >> 12)
+    h = (h * 0x297A2D39) & m
+    h = h ^ (h >> 15)
+    return bk.to_f32(h) * (2.0 / 4294967296.0) - 1.0
+
+
+def _texture(bk, wx, wy, sp: _StreamParams):
+    acc = None
     for k in range(6):
         c, s = math.cos(sp.tex_dirs[k]), math.sin(sp.tex_dirs[k])
-        f = np.float32(2 * math.pi / sp.tex_periods[k])
-        acc += np.sin((wx * np.float32(c) + wy * np.float32(s)) * f + np.float32(sp.tex_phases[k]))
-    gx, gy = wx / np.float32(8.0), wy / np.float32(8.0)
-    ix, iy = np.floor(gx), np.floor(gy)
-    fx, fy = gx - ix, gy - iy
-    ix, iy = ix.astype(np.int64), iy.astype(np.int64)
-    n00 = _hash_u01(ix, iy, sp.lattice_seed)
-    n10 = _hash_u01(ix + 1, iy, sp.lattice_seed)
-    n01 = _hash_u01(ix, iy + 1, sp.lattice_seed)
-    n11 = _hash_u01(ix + 1, iy + 1, sp.lattice_seed)
+        f = 2 * math.pi / sp.tex_periods[k]
+        term = bk.sin((wx * c + wy * s) * f + sp.tex_phases[k])
+        acc = term if acc is None else acc + term
+    gx, gy = wx * 0.125, wy * 0.125
+    fx0, fy0 = bk.floor(gx), bk.floor(gy)
+    fx, fy = gx - fx0, gy - fy0
+    ix, iy = bk.i64(fx0) & 0xFFFFFFFF, bk.i64(fy0) & 0xFFFFFFFF
+    n00 = _hash_u01(bk, ix, iy, sp.lattice_seed)
+    n10 = _hash_u01(bk, (ix + 1) & 0xFFFFFFFF, iy, sp.lattice_seed)
+    n01 = _hash_u01(bk, ix, (iy + 1) & 0xFFFFFFFF, sp.lattice_seed)
+    n11 = _hash_u01(bk, (ix + 1) & 0xFFFFFFFF, (iy + 1) & 0xFFFFFFFF, sp.lattice_seed)
     noise = (n00 * (1 - fx) + n10 * fx) * (1 - fy) + (n01 * (1 - fx) + n11 * fx) * fy
-    t = np.clip(np.float32(0.25) * acc + np.float32(0.45) * noise, -1.0, 1.0)
-    return np.float32(125.0) + np.float32(95.0) * t
+    t = bk.clip(acc * 0.25 + noise * 0.45, -1.0, 1.0)
+    return t * 95.0 + 125.0
 
 
 def _reflect(x: float, lo: float, hi: float) -> float:
@@ -263,31 +347,50 @@ def _object_pos(cfg: SeqConfig, o: dict, t: int) -> np.ndarray:
 
 
 def render_frame(cfg: SeqConfig, sp: _StreamParams, t: int, s: int = 0,
-                 want_gt: bool = False):
-    """Render frame t of a stream: returns (u8 [H][W], gt u8 [H][W] or None)."""
+                 want_gt: bool = False, backend=None):
+    """Render frame t of a stream: returns (u8 [H][W], gt u8 [H][W] or None).
+
+    backend: None/numpy (default, the parity-test reference) or a torch device string.
+    """
+    bk = _NUMPY if backend is None or backend == "numpy" else _Torch(backend)
     P = camera_pose(cfg, sp, t)
-    xs = np.arange(cfg.W, dtype=np.float64) + 0.5
-    ys = np.arange(cfg.H, dtype=np.float64) + 0.5
-    X, Y = np.meshgrid(xs, ys)
-    w = P[2, 0] * X + P[2, 1] * Y + P[2, 2]
-    wx = ((P[0, 0] * X + P[0, 1] * Y + P[0, 2]) / w).astype(np.float32)
-    wy = ((P[1, 0] * X + P[1, 1] * Y + P[1, 2]) / w).astype(np.float32)
-    img = _texture(wx, wy, sp)
-    gt = np.zeros((cfg.H, cfg.W), np.uint8) if want_gt else None
+    X, Y = bk.grid(cfg.W, cfg.H)
+    w = X * P[2, 0] + Y * P[2, 1] + P[2, 2]
+    wx = bk.to_f32((X * P[0, 0] + Y * P[0, 1] + P[0, 2]) / w)
+    wy = bk.to_f32((X * P[1, 0] + Y * P[1, 1] + P[1, 2]) / w)
+    img = _texture(bk, wx, wy, sp)
+    gt = bk.zeros_u8(cfg.H, cfg.W) if want_gt else None
     for o in sp.objects:
         c = _object_pos(cfg, o, t)
         if o["kind"] == "disc":
             inside = (X - c[0]) ** 2 + (Y - c[1]) ** 2 <= (o["w"] / 2) ** 2
         else:
-            inside = (np.abs(X - c[0]) <= o["w"] / 2) & (np.abs(Y - c[1]) <= o["h"] / 2)
-        img[inside] = o["I"]
+            inside = (bk.abs(X - c[0]) <= o["w"] / 2) & (bk.abs(Y - c[1]) <= o["h"] / 2)
+        img[inside] = float(o["I"])
         if want_gt:
             gt[inside] = 255
     if cfg.noise > 0:
-        nrng = np.random.default_rng((sp.noise_seed, t))
-        img = img + nrng.normal(0.0, cfg.noise, img.shape).astype(np.float32)
-    out = np.clip(np.rint(img), 0, 255).astype(np.uint8)
-    return out, gt
+        img = img + bk.noise((sp.noise_seed, t), tuple(img.shape), cfg.noise)
+    return bk.to_u8(img), gt
+
+
+def generate_device(cfg, T: Optional[int] = None, streams=None, device: str = "cuda"):
+    """Fast torch variant of generate() for the bench: (frames u8 [T][S'][H][W] on `device`,
+    homographies f64 [T][S'][9] numpy).  Same recipe; pixel values differ from the numpy
+    backend in rounding and noise draws (bench inputs are not parity references)."""
+    import torch
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    T = cfg.T if T is None else T
+    streams = list(range(cfg.S)) if streams is None else list(streams)
+    frames = torch.empty((T, len(streams), cfg.H, cfg.W), dtype=torch.uint8, device=device)
+    Hs = np.empty((T, len(streams), 9))
+    for j, s in enumerate(streams):
+        sp = _stream_params(cfg, s)
+        Hs[:, j] = homographies_for_stream(cfg, s, T, sp)
+        for t in range(T):
+            frames[t, j] = render_frame(cfg, sp, t, s, False, backend=device)[0]
+    return frames, Hs
 
 
 def generate(cfg, T: Optional[int] = None, streams=None, with_gt: bool = False) -> Sequence:

@@ -1,0 +1,93 @@
+// Host build of the kernel's byte-SWAR and cut-point helpers (csrc/dmsgm_math.cuh),
+// checked against the literal per-pixel predicate of App. E P:657 (reading R14).
+// Built and run by tests/test_host_math.py with g++ -ffp-contract=off.
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <random>
+
+#include "dmsgm_math.cuh"
+
+using namespace dmsgm;
+
+static int check_interval(float mu, float T, float r, long long* fails) {
+    const Interval iv = bg_interval(mu, T, r);
+    uint8_t got[256];
+    for (int I = 0; I < 256; I += 4) {
+        uint32_t px = (uint32_t)I | ((uint32_t)(I + 1) << 8) | ((uint32_t)(I + 2) << 16) | ((uint32_t)(I + 3) << 24);
+        uint32_t a4 = (uint32_t)iv.a * 0x01010101u, w4 = (uint32_t)iv.w * 0x01010101u;
+        uint32_t f4 = iv.empty ? 0xFFFFFFFFu : 0u;
+        uint32_t m = mask_bytes(px, a4, w4, f4);
+        for (int j = 0; j < 4; ++j) got[I + j] = (m >> (8 * j)) & 0xFF;
+    }
+    int bad = 0;
+    for (int I = 0; I < 256; ++I) {
+        const uint8_t expect = fg_pred((float)I, mu, T) ? 255 : 0;
+        if (got[I] != expect) ++bad;
+    }
+    if (bad) {
+        if (*fails < 10)
+            printf("MISMATCH mu=%.9g T=%.9g r=%.9g a=%d w=%d empty=%d bad=%d\n", mu, T, r, iv.a, iv.w,
+                   (int)iv.empty, bad);
+        ++*fails;
+    }
+    return bad;
+}
+
+int main(int argc, char** argv) {
+    long long trials = argc > 1 ? atoll(argv[1]) : 2000000;
+    long long fails = 0;
+    // 1) SWAR primitives, every byte pair in every lane
+    std::mt19937 rng(1234);
+    long long swar_bad = 0;
+    for (int x = 0; x < 256; ++x)
+        for (int y = 0; y < 256; ++y)
+            for (int lane = 0; lane < 4; ++lane) {
+                uint32_t X = rng(), Y = rng();
+                X = (X & ~(0xFFu << (8 * lane))) | ((uint32_t)x << (8 * lane));
+                Y = (Y & ~(0xFFu << (8 * lane))) | ((uint32_t)y << (8 * lane));
+                uint32_t d = (sub_bytes(X, Y) >> (8 * lane)) & 0xFF;
+                uint32_t g = (gt_bytes(X, Y) >> (8 * lane)) & 0xFF;
+                if (d != (uint32_t)((x - y) & 0xFF)) ++swar_bad;
+                if (g != (x > y ? 0xFFu : 0u)) ++swar_bad;
+            }
+    printf("swar_bad %lld\n", swar_bad);
+
+    // 2) background intervals: random and adversarial (mu, T), sqrt estimates off by a few ulp
+    std::uniform_real_distribution<float> U(0.f, 1.f);
+    const float thetas[] = {4.f, 1.f, 9.f, 2.5f, 16.f};
+    for (long long t = 0; t < trials; ++t) {
+        float mu;
+        const int kind = (int)(t % 6);
+        if (kind == 0) mu = 255.f * U(rng);
+        else if (kind == 1) mu = (float)(int)(256.f * U(rng));                  // integer mean
+        else if (kind == 2) mu = (float)(int)(255.f * U(rng)) + 0.5f;           // half-integer
+        else if (kind == 3) mu = nextafterf((float)(int)(256.f * U(rng)), U(rng) < 0.5f ? 0.f : 300.f);
+        else if (kind == 4) mu = U(rng) < 0.5f ? 255.f * U(rng) * U(rng) * U(rng) : 255.f - 255.f * U(rng) * U(rng) * U(rng);
+        else mu = 255.00003f * U(rng);
+        if (mu > 255.f && kind != 5) mu = 255.f;
+        float var;
+        const int vk = (int)((t / 6) % 4);
+        if (vk == 0) var = expf(logf(1e-4f) + (logf(1e6f) - logf(1e-4f)) * U(rng));
+        else if (vk == 1) var = 0.25f * U(rng);
+        else if (vk == 2) var = (float)(int)(2000.f * U(rng)) * 0.25f;
+        else var = 65025.f * U(rng);
+        const float theta = thetas[(t / 24) % 5];
+        float T = theta * (var > 0.25f ? var : 0.25f);
+        if ((t & 7) == 7) {
+            // T exactly at fl(fl(k - mu)^2) for some k, or one ulp either side
+            int k = (int)(256.f * U(rng));
+            float d = f_sub((float)k, mu);
+            T = f_mul(d, d);
+            int side = (int)(3.f * U(rng));
+            if (side == 1) T = nextafterf(T, 0.f);
+            if (side == 2) T = nextafterf(T, INFINITY);
+            if (!(T > 0.f)) T = 1e-6f;
+        }
+        const float sq = sqrtf(T);
+        const float r = sq * (1.0f + (U(rng) - 0.5f) * 4e-6f);
+        check_interval(mu, T, r, &fails);
+    }
+    printf("interval_fails %lld of %lld\n", fails, trials);
+    return (swar_bad || fails) ? 1 : 0;
+}
