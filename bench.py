@@ -268,10 +268,12 @@ def run_dmsgm(args, rank, world, local):
     ev1 = torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     with sampler:
+        torch.cuda.nvtx.range_push("timed")
         ev0.record(stream)
         for i in range(args.steps):
             step(args.warmup + i)
         ev1.record(stream)
+        torch.cuda.nvtx.range_pop()
         sampler.sample_once()
         ev1.synchronize()
     torch.cuda.synchronize(dev)

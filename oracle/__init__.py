@@ -67,6 +67,8 @@ def _load():
             lib.dmsgm_oracle_set_state.argtypes = [P, i32, P]
             lib.dmsgm_oracle_is_initialised.argtypes = [P, i32]
             lib.dmsgm_oracle_mix_weights.argtypes = [i32, i32, i32, P, i32, i32, P, P, P, P]
+            lib.dmsgm_oracle_decay_exp.argtypes = [ctypes.c_float]
+            lib.dmsgm_oracle_decay_exp.restype = ctypes.c_float
             _lib = lib
     return _lib
 
@@ -162,8 +164,13 @@ class Oracle:
         return bool(self.lib.dmsgm_oracle_is_initialised(self._h, stream))
 
 
-def mix_weights(width: int, height: int, block: int, h, bi: int, bj: int):
-    """Step S1 for one block: (exposed, src [(x,y)]*4, weights f32[4], sumW)."""
+def decay_exp(x: float) -> float:
+    """exp(-x) as the oracle evaluates it (reading R18)."""
+    return float(_load().dmsgm_oracle_decay_exp(x))
+
+
+def mix_weights(width: int, height: int, block: int, h, bi: int, bj: int, with_clipped: bool = False):
+    """Step S1 for one block: (exposed, src [(x,y)]*4, raw weights f32[4], sumW[, clipped])."""
     lib = _load()
     hh = np.ascontiguousarray(np.asarray(h, np.float64).reshape(9))
     sx = np.zeros(4, np.int32)
@@ -174,7 +181,8 @@ def mix_weights(width: int, height: int, block: int, h, bi: int, bj: int):
                                       _ptr(w), _ptr(sw))
     if rc < 0:
         raise ValueError("bad arguments")
-    return bool(rc), list(zip(sx.tolist(), sy.tolist())), w, float(sw[0])
+    out = (rc == 1, list(zip(sx.tolist(), sy.tolist())), w, float(sw[0]))
+    return out + (rc == 2,) if with_clipped else out
 
 
 def run_sequence(frames: np.ndarray, homographies: np.ndarray, block: int,

@@ -16,7 +16,7 @@
  *   mask          App. E P:655-663 with the variance reading R14.
  *
  * Arithmetic: fp32 state (north_star: "fp32 means/variances"), fp64 for the
- * projection and exp only (R17/R18).  Built with -O2 -ffp-contract=off
+ * projection only (R17); the decay exp is a fixed fp32 sequence (R18).  Built with -O2 -ffp-contract=off
  * -fno-fast-math: every + - * / below is one IEEE round-to-nearest operation,
  * evaluated in the order written, no FMA contraction.  x*x is used, never pow.
  *
@@ -59,7 +59,7 @@ static float* stream_state(const dmsgm_oracle_ctx* c, int buf, int s) {
  * in-range source has weight).  Returns 1 if exposed.
  * ---------------------------------------------------------------------- */
 static int project_block(int Wb, int Hb, int N, const double* h, int bi, int bj,
-                         int kx[4], int ky[4], float Wt[4], float* sumW) {
+                         int kx[4], int ky[4], float Wt[4], float* sumW, int* clipped) {
     double X = (double)N * (double)bi + (double)N / 2.0; /* block centre, R2 */
     double Y = (double)N * (double)bj + (double)N / 2.0;
     double w = h[6] * X;
@@ -96,8 +96,12 @@ static int project_block(int Wb, int Hb, int N, const double* h, int bi, int bj,
     kx[1] = (int)ku + su;  ky[1] = (int)kv;
     kx[2] = (int)ku;       ky[2] = (int)kv + sv;
     kx[3] = (int)ku + su;  ky[3] = (int)kv + sv;
+    *clipped = 0;
     for (int k = 0; k < 4; ++k)
-        if (kx[k] < 0 || kx[k] >= Wb || ky[k] < 0 || ky[k] >= Hb) Wt[k] = 0.0f;
+        if (kx[k] < 0 || kx[k] >= Wb || ky[k] < 0 || ky[k] >= Hb) {
+            if (Wt[k] > 0.0f) *clipped = 1;   /* part of the footprint lies outside the grid */
+            Wt[k] = 0.0f;
+        }
     float sw = Wt[0] + Wt[1];
     sw = sw + Wt[2];
     sw = sw + Wt[3];
@@ -107,14 +111,39 @@ static int project_block(int Wb, int Hb, int N, const double* h, int bi, int bj,
 }
 
 /* ------------------------------------------------------------------------
+ * R18: exp(-x) for x >= 0 in fp32 by one fixed sequence of IEEE operations
+ * (so that any two IEEE machines agree bitwise):
+ *   n = rint(x * log2 e);  r = (x - n*L1) - n*L2   (L1 + L2 = ln 2; L1 has 16
+ *   significant bits, so n*L1 is exact for n < 128);
+ *   p = sum_{k=0..7} (-r)^k / k!  by Horner from k = 7 down;   exp(-x) = p * 2^-n.
+ * x >= 86 returns 0 (exp(-86) is within 3 binades of FLT_MIN).
+ * ---------------------------------------------------------------------- */
+static float decay_exp(float x) {
+    if (!(x < 86.0f)) return 0.0f;
+    const float n = rintf(x * 1.44269502f);
+    float r = x - n * 0.693145751953125f;
+    r = r - n * 1.42860677e-06f;
+    float p = -1.98412701e-04f;            /* -1/7! */
+    p = p * r + 1.38888892e-03f;           /*  1/6! */
+    p = p * r + -8.33333377e-03f;          /* -1/5! */
+    p = p * r + 4.16666679e-02f;           /*  1/4! */
+    p = p * r + -1.66666672e-01f;          /* -1/3! */
+    p = p * r + 0.5f;                      /*  1/2! */
+    p = p * r + -1.0f;                     /* -1/1! */
+    p = p * r + 1.0f;                      /*  1/0! */
+    return p * ldexpf(1.0f, -(int)n);
+}
+
+/* ------------------------------------------------------------------------
  * S2: mix one model (A with A, C with C) over the sources, reading R6:
- *   w_k = W_k / sum W                       (normalised overlap areas)
+ *   w_k = W_k                               (overlap areas of the unit footprint), or
+ *   w_k = W_k / sum W  if part of the footprint fell outside the grid (renormalised)
  *   mu~  = sum_k w_k mu_k
  *   var~ = sum_k w_k (var_k + (mu~ - mu_k)^2)   (mixture second moment about mu~)
  *   age~ = min(sum_k w_k age_k, cap)
  * Sums run over in-range sources in the order self, H, V, HV.
  * S3: age decay (R7): if lambda > 0 and var~ > theta_v,
- *   age~ <- age~ * exp(-lambda (var~ - theta_v)).
+ *   age~ <- age~ * exp(-lambda (var~ - theta_v))   with exp as in decay_exp (R18).
  * ---------------------------------------------------------------------- */
 static sgm mix_model(const dmsgm_oracle_ctx* c, const float* prev, int pm, const int kx[4],
                      const int ky[4], const float wn[4], const int valid[4]) {
@@ -150,8 +179,8 @@ static sgm mix_model(const dmsgm_oracle_ctx* c, const float* prev, int pm, const
     /* S3 */
     if (c->p.decay_lambda > 0.0f && m.var > c->p.decay_var_thresh) {
         float excess = m.var - c->p.decay_var_thresh;
-        double f = exp(-(double)c->p.decay_lambda * (double)excess);
-        m.age = m.age * (float)f;
+        float x = c->p.decay_lambda * excess;
+        m.age = m.age * decay_exp(x);
     }
     return m;
 }
@@ -170,17 +199,19 @@ static float block_V(float mu, const uint8_t* frame, size_t pitch, int x0, int y
     return V;
 }
 
-/* Eqs. 3, 5, 6, 7 for a matched model (R10: incremental form of Eq. 3/5,
- * mu = mu~ + (M - mu~)/(alpha~+1); R22: alpha = min(alpha~+1, cap)), or the
+/* Eqs. 3, 5, 6, 7 for a matched model (R10: incremental form of Eq. 3/5 with
+ * the learning rate 1/(alpha~+1) computed once, mu = mu~ + (M - mu~)*rate;
+ * R22: alpha = min(alpha~+1, cap)), or the
  * App. E code rule when update_rule == 1 (R27). */
 static sgm update_model(const dmsgm_oracle_ctx* c, sgm t, float M, const uint8_t* frame,
                         size_t pitch, int x0, int y0) {
     sgm r;
     if (c->p.update_rule == 0) {
         float den = t.age + 1.0f;
-        r.mu = t.mu + (M - t.mu) / den;                                  /* Eq. 3 */
+        float rate = 1.0f / den;                                         /* 1/(alpha~+1) */
+        r.mu = t.mu + (M - t.mu) * rate;                                 /* Eq. 3 */
         float V = block_V(r.mu, frame, pitch, x0, y0, c->N);             /* Eq. 6 */
-        r.var = t.var + (V - t.var) / den;                               /* Eq. 5 */
+        r.var = t.var + (V - t.var) * rate;                              /* Eq. 5 */
         r.age = den < c->p.age_cap ? den : c->p.age_cap;                 /* Eq. 7 + cap */
     } else {
         float age = t.age > 1.0f ? t.age : 1.0f;
@@ -216,14 +247,14 @@ static int step_stream(dmsgm_oracle_ctx* c, int s, const uint8_t* frame, size_t 
             int exposed = !initialised; /* R8: first frame of a stream */
             sgm At = fresh_tmpl, Ct = fresh_tmpl;
             if (!exposed) {
-                int kx[4], ky[4], valid[4];
+                int kx[4], ky[4], valid[4], clipped;
                 float Wt[4], sumW;
-                exposed = project_block(Wb, Hb, N, h, bi, bj, kx, ky, Wt, &sumW);   /* S1 */
+                exposed = project_block(Wb, Hb, N, h, bi, bj, kx, ky, Wt, &sumW, &clipped);   /* S1 */
                 if (!exposed) {
                     float wn[4];
                     for (int k = 0; k < 4; ++k) {
                         valid[k] = Wt[k] != 0.0f;
-                        wn[k] = Wt[k] / sumW;
+                        wn[k] = clipped ? Wt[k] / sumW : Wt[k];                            /* R6 */
                     }
                     At = mix_model(c, prev, P_MU_A, kx, ky, wn, valid);           /* S2+S3 */
                     Ct = mix_model(c, prev, P_MU_C, kx, ky, wn, valid);
@@ -388,5 +419,10 @@ int dmsgm_oracle_mix_weights(int width, int height, int block, const double* h, 
                              int* src_x, int* src_y, float* weight, float* sum_w) {
     if (!h || !src_x || !src_y || !weight || !sum_w) return -1;
     if (block < 1 || width % block || height % block) return -1;
-    return project_block(width / block, height / block, block, h, bi, bj, src_x, src_y, weight, sum_w);
+    int clipped = 0;
+    int r = project_block(width / block, height / block, block, h, bi, bj, src_x, src_y, weight, sum_w,
+                          &clipped);
+    return r ? 1 : (clipped ? 2 : 0);
 }
+
+float dmsgm_oracle_decay_exp(float x) { return decay_exp(x); }

@@ -63,10 +63,15 @@ int dmsgm_oracle_is_initialised(const dmsgm_oracle_ctx* ctx, int stream);
 
 /* Step S1 alone for block (bi, bj) under homography h[9] (exposed for the
  * polygon-overlap pin P12).  Returns 1 if the block is exposed (R5), else 0
- * and fills src_x[4], src_y[4] (source block indices, order self/H/V/HV),
- * weight[4] (raw overlap weights, out-of-range sources zeroed) and *sum_w. */
+ * (footprint inside the grid) or 2 (footprint clipped by the border: the step
+ * renormalises by *sum_w, R6), and fills src_x[4], src_y[4] (source block
+ * indices, order self/H/V/HV), weight[4] (raw overlap areas, out-of-range
+ * sources zeroed) and *sum_w. */
 int dmsgm_oracle_mix_weights(int width, int height, int block, const double* h, int bi, int bj,
                              int* src_x, int* src_y, float* weight, float* sum_w);
+
+/* The decay factor exp(-x) of reading R18 (exposed for its pin). */
+float dmsgm_oracle_decay_exp(float x);
 
 #ifdef __cplusplus
 }

@@ -108,12 +108,19 @@ KParams kparams(const dmsgm_params& p) {
 
 size_t plane_elems(const dmsgm_ctx* c) { return (size_t)c->Wb * (size_t)c->Hb; }
 
-int strips_of(const dmsgm_ctx* c) {
+// Blocks per thread strip: a strip row must be 4, 8 or 16 bytes (N*BPT), and Wb % BPT == 0.
+int bpt_of(const dmsgm_ctx* c) {
     switch (c->N) {
-        case 1: return c->Wb / Geom<1>::BPT;
-        case 2: return c->Wb / Geom<2>::BPT;
-        default: return c->Wb;
+        case 1: return 4;
+        case 2: return 2;
+        case 4: return (c->Wb % 2 == 0) ? 2 : 1;
+        default: return 1;
     }
+}
+
+template <int N, int BPT>
+void launch_kernel(const StepArgs& a, dim3 grid, dim3 block, cudaStream_t stream) {
+    dmsgm_step_kernel<N, BPT><<<grid, block, 0, stream>>>(a);
 }
 
 // Enqueue one kernel for streams [s0, s0+count) of the batch.
@@ -123,11 +130,11 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     StepArgs a;
     a.frames = frames;
     a.fstride = (long long)c->H * (long long)fpitch;
-    a.fpitch = (long long)fpitch;
+    a.fpitch = (int)fpitch;
+    a.mpitch = (int)mpitch;
     a.H = H;
     a.masks = masks;
     a.mstride = (long long)c->H * (long long)mpitch;
-    a.mpitch = (long long)mpitch;
     const size_t sstride = 6 * plane_elems(c);
     a.prev = c->state[parity] + (size_t)s0 * sstride;
     a.next = c->state[parity ^ 1] + (size_t)s0 * sstride;
@@ -135,17 +142,19 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     a.fresh_out = c->fresh[parity ^ 1] + s0;
     a.Wb = c->Wb;
     a.Hb = c->Hb;
-    a.Wstrips = strips_of(c);
-    a.plane = (long long)plane_elems(c);
+    const int bpt = bpt_of(c);
+    a.Wstrips = c->Wb / bpt;
+    a.plane = (int)plane_elems(c);
     a.kp = kparams(c->p);
     dim3 block(kCtaX, kCtaY, 1);
     dim3 grid((a.Wstrips + kCtaX - 1) / kCtaX, (c->Hb + kCtaY - 1) / kCtaY, count);
-    switch (c->N) {
-        case 1: dmsgm_step_kernel<1><<<grid, block, 0, stream>>>(a); break;
-        case 2: dmsgm_step_kernel<2><<<grid, block, 0, stream>>>(a); break;
-        case 4: dmsgm_step_kernel<4><<<grid, block, 0, stream>>>(a); break;
-        case 8: dmsgm_step_kernel<8><<<grid, block, 0, stream>>>(a); break;
-        case 16: dmsgm_step_kernel<16><<<grid, block, 0, stream>>>(a); break;
+    switch (c->N * 16 + bpt) {
+        case 1 * 16 + 4: launch_kernel<1, 4>(a, grid, block, stream); break;
+        case 2 * 16 + 2: launch_kernel<2, 2>(a, grid, block, stream); break;
+        case 4 * 16 + 2: launch_kernel<4, 2>(a, grid, block, stream); break;
+        case 4 * 16 + 1: launch_kernel<4, 1>(a, grid, block, stream); break;
+        case 8 * 16 + 1: launch_kernel<8, 1>(a, grid, block, stream); break;
+        case 16 * 16 + 1: launch_kernel<16, 1>(a, grid, block, stream); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -159,6 +168,8 @@ int check_images(dmsgm_ctx* c, const void* frames, size_t fpitch, const void* H,
     if ((uintptr_t)H & 7) return fail(c, DMSGM_EINVAL, "homographies must be 8-byte aligned");
     if (fpitch < (size_t)c->W || (fpitch & 15)) return fail(c, DMSGM_EINVAL, "frame_pitch must be >= width and a multiple of 16");
     if (mpitch < (size_t)c->W || (mpitch & 15)) return fail(c, DMSGM_EINVAL, "mask_pitch must be >= width and a multiple of 16");
+    if ((double)fpitch * c->H > 2147483647.0 || (double)mpitch * c->H > 2147483647.0)
+        return fail(c, DMSGM_EINVAL, "one image (pitch x height) must be < 2 GiB");
     return DMSGM_OK;
 }
 
@@ -186,6 +197,8 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
     if (width <= 0 || height <= 0 || width % block || height % block)
         return fail(nullptr, DMSGM_EINVAL, "width/height must be positive multiples of block (R1)");
     if (width % 4) return fail(nullptr, DMSGM_EINVAL, "width must be a multiple of 4");
+    if ((double)(width / block) * (height / block) * 6.0 > 2147483647.0)
+        return fail(nullptr, DMSGM_EINVAL, "block grid too large (6*Wb*Hb must be < 2^31)");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess) return fail(nullptr, DMSGM_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));

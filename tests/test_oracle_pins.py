@@ -374,7 +374,7 @@ def test_decay_closed_form(oracle_mod):
     N = 2
     st = _state_from(1, 1, [100.0, 3500.0, 10.0], [3.0, 1.0, 1.0])
     A, _ = _probe_tilde_A(oracle_mod, st, IDENT, N, N, N, decay_lambda=0.001, decay_var_thresh=2500.0)
-    assert _ulps(A[2, 0, 0], 10.0 * math.exp(-1.0)) <= 1
+    assert _ulps(A[2, 0, 0], 10.0 * math.exp(-1.0)) <= 3
     assert A[1, 0, 0] == 3500.0 and A[0, 0, 0] == 100.0
     # at or below the threshold: no decay
     st = _state_from(1, 1, [100.0, 2500.0, 10.0], [3.0, 1.0, 1.0])
@@ -470,3 +470,50 @@ def test_appendix_classify_rule(oracle_mod):
     _, mask = _one_step(oracle_mod, frame, st, N, theta_s=1e-30, classify_rule=1)
     # 18^2=324 > 80 fg; 19^2=361 > 84 fg; 2^2=4 <= 16 bg; 2^2=4 > 4*0.25=1 fg
     assert mask.tolist() == [[255, 255], [0, 255]]
+
+
+# --------------------------------------------------------------------------
+# R18: the fixed-sequence fp32 exp(-x) against libm (double), and its cut-off
+# --------------------------------------------------------------------------
+def test_decay_exp_accuracy(oracle_mod):
+    xs = np.concatenate([np.linspace(0.0, 85.99, 40001), np.exp(np.linspace(-20, 4.45, 2000)),
+                         np.array([0.0, 1e-30, 0.34657359, 0.34657360, 1.0, 2.5, 60.0])])
+    worst = 0.0
+    for x in xs:
+        x32 = float(np.float32(x))
+        got = oracle_mod.decay_exp(x32)
+        ref = math.exp(-x32)
+        worst = max(worst, abs(got - ref) / ref)
+    assert worst < 3.0e-7, worst          # ~2.5 fp32 ulp at worst
+    assert oracle_mod.decay_exp(0.0) == 1.0
+    assert oracle_mod.decay_exp(86.0) == 0.0 and oracle_mod.decay_exp(1e9) == 0.0
+
+
+# --------------------------------------------------------------------------
+# R6: renormalisation only when the footprint is clipped by the grid border
+# --------------------------------------------------------------------------
+def test_clipped_renormalisation(oracle_mod):
+    N, W, Hh = 4, 32, 16
+    Wb, Hb = W // N, Hh // N
+    # interior footprint (quarter-block shift): not clipped, raw areas are the weights
+    H = np.array([1.0, 0.0, 1.0, 0.0, 1.0, 1.0, 0.0, 0.0, 1.0])
+    e, src, w, sw, clipped = oracle_mod.mix_weights(W, Hh, N, H, 3, 2, with_clipped=True)
+    assert not e and not clipped
+    assert w.tolist() == [0.5625, 0.1875, 0.1875, 0.0625] and sw == 1.0
+    # last column: the H-neighbour falls outside -> clipped, sum of in-range areas 0.75
+    e, src, w, sw, clipped = oracle_mod.mix_weights(W, Hh, N, H, Wb - 1, 2, with_clipped=True)
+    assert not e and clipped and sw == 0.75
+    # identity at the border: zero-weight neighbours outside do not count as clipping
+    e, src, w, sw, clipped = oracle_mod.mix_weights(W, Hh, N, IDENT, Wb - 1, Hb - 1, with_clipped=True)
+    assert not e and not clipped
+    # through the step: last-column tilde = (0.5625 mu_s + 0.1875 mu_v) / 0.75 etc.
+    st = np.zeros((6, Hb, Wb), np.float32)
+    st[0] = np.arange(Wb * Hb, dtype=np.float32).reshape(Hb, Wb) * 3.0
+    st[1] = 8.0
+    st[2] = 12.0
+    st[3:6] = st[0:3]
+    A, _ = _probe_tilde_A(oracle_mod, st, H, N, W, Hh)
+    mu_s, mu_v = st[0, 2, Wb - 1], st[0, 3, Wb - 1]
+    expect_mu = (0.5625 / 0.75) * mu_s + (0.1875 / 0.75) * mu_v
+    assert abs(A[0, 2, Wb - 1] - expect_mu) < 1e-4
+    assert abs(A[2, 2, Wb - 1] - 12.0) < 1e-5
