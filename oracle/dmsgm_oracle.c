@@ -16,9 +16,11 @@
  *   mask          App. E P:655-663 with the variance reading R14.
  *
  * Arithmetic: fp32 state (north_star: "fp32 means/variances"), fp64 for the
- * projection only (R17); the decay exp is a fixed fp32 sequence (R18).  Built with -O2 -ffp-contract=off
- * -fno-fast-math: every + - * / below is one IEEE round-to-nearest operation,
- * evaluated in the order written, no FMA contraction.  x*x is used, never pow.
+ * projection only (R17); the decay exp is a fixed fp32 sequence (R18).  Built
+ * with -O2 -ffp-contract=off -fno-fast-math: every + - * / below is one IEEE
+ * round-to-nearest operation evaluated in the order written; fused
+ * multiply-adds appear only where written as fma()/fmaf() (correctly rounded,
+ * C99), never by contraction.  x*x is used, never pow.
  *
  * Layout: state [S][6][Hb][Wb] fp32, planes mu_A var_A age_A mu_C var_C age_C.
  */
@@ -62,18 +64,15 @@ static int project_block(int Wb, int Hb, int N, const double* h, int bi, int bj,
                          int kx[4], int ky[4], float Wt[4], float* sumW, int* clipped) {
     double X = (double)N * (double)bi + (double)N / 2.0; /* block centre, R2 */
     double Y = (double)N * (double)bj + (double)N / 2.0;
-    double w = h[6] * X;
-    w = w + h[7] * Y;
-    w = w + h[8];
+    /* homogeneous image of the centre: (xn, yn, w) = H (X, Y, 1), each row as
+     * h_i0*X + (h_i1*Y + h_i2) with fused multiply-adds (R17) */
+    double w = fma(h[6], X, fma(h[7], Y, h[8]));
     if (!(w > 0.0)) return 1;
-    double xn = h[0] * X;
-    xn = xn + h[1] * Y;
-    xn = xn + h[2];
-    double yn = h[3] * X;
-    yn = yn + h[4] * Y;
-    yn = yn + h[5];
-    double xp = xn / w; /* frame t-1 pixel coordinates of the centre */
-    double yp = yn / w;
+    double xn = fma(h[0], X, fma(h[1], Y, h[2]));
+    double yn = fma(h[3], X, fma(h[4], Y, h[5]));
+    double rw = 1.0 / w;
+    double xp = xn * rw; /* frame t-1 pixel coordinates of the centre */
+    double yp = yn * rw;
     double u = xp / (double)N; /* source block-grid coordinates: block k covers [k, k+1) */
     double v = yp / (double)N;
     if (!(u > -2.0 && u < (double)Wb + 2.0 && v > -2.0 && v < (double)Hb + 2.0)) return 1;
@@ -113,24 +112,24 @@ static int project_block(int Wb, int Hb, int N, const double* h, int bi, int bj,
 /* ------------------------------------------------------------------------
  * R18: exp(-x) for x >= 0 in fp32 by one fixed sequence of IEEE operations
  * (so that any two IEEE machines agree bitwise):
- *   n = rint(x * log2 e);  r = (x - n*L1) - n*L2   (L1 + L2 = ln 2; L1 has 16
- *   significant bits, so n*L1 is exact for n < 128);
- *   p = sum_{k=0..7} (-r)^k / k!  by Horner from k = 7 down;   exp(-x) = p * 2^-n.
+ *   n = rint(x * log2 e);  r = fma(-n, L1, x); r = fma(-n, L2, r)   (L1 + L2 = ln 2;
+ *   L1 has 16 significant bits, so n*L1 is exact for n < 128);
+ *   p = sum_{k=0..7} (-r)^k / k!  by Horner with fma from k = 7 down;  exp(-x) = p * 2^-n.
  * x >= 86 returns 0 (exp(-86) is within 3 binades of FLT_MIN).
  * ---------------------------------------------------------------------- */
 static float decay_exp(float x) {
     if (!(x < 86.0f)) return 0.0f;
     const float n = rintf(x * 1.44269502f);
-    float r = x - n * 0.693145751953125f;
-    r = r - n * 1.42860677e-06f;
+    float r = fmaf(-n, 0.693145751953125f, x);
+    r = fmaf(-n, 1.42860677e-06f, r);
     float p = -1.98412701e-04f;            /* -1/7! */
-    p = p * r + 1.38888892e-03f;           /*  1/6! */
-    p = p * r + -8.33333377e-03f;          /* -1/5! */
-    p = p * r + 4.16666679e-02f;           /*  1/4! */
-    p = p * r + -1.66666672e-01f;          /* -1/3! */
-    p = p * r + 0.5f;                      /*  1/2! */
-    p = p * r + -1.0f;                     /* -1/1! */
-    p = p * r + 1.0f;                      /*  1/0! */
+    p = fmaf(p, r, 1.38888892e-03f);       /*  1/6! */
+    p = fmaf(p, r, -8.33333377e-03f);      /* -1/5! */
+    p = fmaf(p, r, 4.16666679e-02f);       /*  1/4! */
+    p = fmaf(p, r, -1.66666672e-01f);      /* -1/3! */
+    p = fmaf(p, r, 0.5f);                  /*  1/2! */
+    p = fmaf(p, r, -1.0f);                 /* -1/1! */
+    p = fmaf(p, r, 1.0f);                  /*  1/0! */
     return p * ldexpf(1.0f, -(int)n);
 }
 
@@ -141,7 +140,8 @@ static float decay_exp(float x) {
  *   mu~  = sum_k w_k mu_k
  *   var~ = sum_k w_k (var_k + (mu~ - mu_k)^2)   (mixture second moment about mu~)
  *   age~ = min(sum_k w_k age_k, cap)
- * Sums run over in-range sources in the order self, H, V, HV.
+ * Sums run over in-range sources in the order self, H, V, HV, accumulated with
+ * fused multiply-adds acc = fma(w_k, x_k, acc) from acc = 0 (R17).
  * S3: age decay (R7): if lambda > 0 and var~ > theta_v,
  *   age~ <- age~ * exp(-lambda (var~ - theta_v))   with exp as in decay_exp (R18).
  * ---------------------------------------------------------------------- */
@@ -162,19 +162,19 @@ static sgm mix_model(const dmsgm_oracle_ctx* c, const float* prev, int pm, const
     sgm m;
     float acc = 0.0f;
     for (int k = 0; k < 4; ++k)
-        if (valid[k]) acc = acc + wn[k] * mu_k[k];
+        if (valid[k]) acc = fmaf(wn[k], mu_k[k], acc);
     m.mu = acc;
     acc = 0.0f;
     for (int k = 0; k < 4; ++k) {
         if (!valid[k]) continue;
         float d = m.mu - mu_k[k];
-        float second = var_k[k] + d * d;
-        acc = acc + wn[k] * second;
+        float second = fmaf(d, d, var_k[k]);   /* var_k + (mu~ - mu_k)^2 */
+        acc = fmaf(wn[k], second, acc);
     }
     m.var = acc;
     acc = 0.0f;
     for (int k = 0; k < 4; ++k)
-        if (valid[k]) acc = acc + wn[k] * age_k[k];
+        if (valid[k]) acc = fmaf(wn[k], age_k[k], acc);
     m.age = acc < c->p.age_cap ? acc : c->p.age_cap;
     /* S3 */
     if (c->p.decay_lambda > 0.0f && m.var > c->p.decay_var_thresh) {
@@ -200,7 +200,7 @@ static float block_V(float mu, const uint8_t* frame, size_t pitch, int x0, int y
 }
 
 /* Eqs. 3, 5, 6, 7 for a matched model (R10: incremental form of Eq. 3/5 with
- * the learning rate 1/(alpha~+1) computed once, mu = mu~ + (M - mu~)*rate;
+ * the learning rate 1/(alpha~+1) computed once, mu = fma(M - mu~, rate, mu~);
  * R22: alpha = min(alpha~+1, cap)), or the
  * App. E code rule when update_rule == 1 (R27). */
 static sgm update_model(const dmsgm_oracle_ctx* c, sgm t, float M, const uint8_t* frame,
@@ -209,9 +209,9 @@ static sgm update_model(const dmsgm_oracle_ctx* c, sgm t, float M, const uint8_t
     if (c->p.update_rule == 0) {
         float den = t.age + 1.0f;
         float rate = 1.0f / den;                                         /* 1/(alpha~+1) */
-        r.mu = t.mu + (M - t.mu) * rate;                                 /* Eq. 3 */
+        r.mu = fmaf(M - t.mu, rate, t.mu);                               /* Eq. 3 */
         float V = block_V(r.mu, frame, pitch, x0, y0, c->N);             /* Eq. 6 */
-        r.var = t.var + (V - t.var) * rate;                              /* Eq. 5 */
+        r.var = fmaf(V - t.var, rate, t.var);                            /* Eq. 5 */
         r.age = den < c->p.age_cap ? den : c->p.age_cap;                 /* Eq. 7 + cap */
     } else {
         float age = t.age > 1.0f ? t.age : 1.0f;

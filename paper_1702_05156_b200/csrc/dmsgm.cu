@@ -21,6 +21,7 @@ using namespace dmsgm;
 namespace {
 
 constexpr int kPipeStreams = 3;
+constexpr int kRowsPerCta = 4;
 
 struct GraphSlot {
     bool valid = false;
@@ -107,6 +108,30 @@ KParams kparams(const dmsgm_params& p) {
 }
 
 size_t plane_elems(const dmsgm_ctx* c) { return (size_t)c->Wb * (size_t)c->Hb; }
+int tiles_x_of(const dmsgm_ctx* c) { return (c->Wb + kTile - 1) / kTile; }
+// floats of one stream's state in the internal AoSoA layout [Hb][tiles_x][6][32]
+size_t stream_floats(const dmsgm_ctx* c) { return (size_t)c->Hb * tiles_x_of(c) * kTileFloats; }
+
+// public [6][Hb][Wb] <-> internal [Hb][tiles_x][6][32] (host side, not on the hot path)
+void to_public(const dmsgm_ctx* c, const float* in, float* out) {
+    const size_t pe = plane_elems(c);
+    const int tx = tiles_x_of(c);
+    for (int p = 0; p < 6; ++p)
+        for (int by = 0; by < c->Hb; ++by)
+            for (int bx = 0; bx < c->Wb; ++bx)
+                out[p * pe + (size_t)by * c->Wb + bx] =
+                    in[((size_t)by * tx + bx / kTile) * kTileFloats + p * kTile + bx % kTile];
+}
+void to_internal(const dmsgm_ctx* c, const float* in, float* out) {
+    const size_t pe = plane_elems(c);
+    const int tx = tiles_x_of(c);
+    memset(out, 0, stream_floats(c) * sizeof(float));
+    for (int p = 0; p < 6; ++p)
+        for (int by = 0; by < c->Hb; ++by)
+            for (int bx = 0; bx < c->Wb; ++bx)
+                out[((size_t)by * tx + bx / kTile) * kTileFloats + p * kTile + bx % kTile] =
+                    in[p * pe + (size_t)by * c->Wb + bx];
+}
 
 // Blocks per thread strip: a strip row must be 4, 8 or 16 bytes (N*BPT), and Wb % BPT == 0.
 int bpt_of(const dmsgm_ctx* c) {
@@ -135,7 +160,7 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     a.H = H;
     a.masks = masks;
     a.mstride = (long long)c->H * (long long)mpitch;
-    const size_t sstride = 6 * plane_elems(c);
+    const size_t sstride = stream_floats(c);
     a.prev = c->state[parity] + (size_t)s0 * sstride;
     a.next = c->state[parity ^ 1] + (size_t)s0 * sstride;
     a.fresh_in = c->fresh[parity] + s0;
@@ -144,10 +169,13 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     a.Hb = c->Hb;
     const int bpt = bpt_of(c);
     a.Wstrips = c->Wb / bpt;
-    a.plane = (int)plane_elems(c);
+    a.tiles_x = tiles_x_of(c);
+    a.sstride = (int)sstride;
     a.kp = kparams(c->p);
     dim3 block(kCtaX, kCtaY, 1);
-    dim3 grid((a.Wstrips + kCtaX - 1) / kCtaX, (c->Hb + kCtaY - 1) / kCtaY, count);
+    // each CTA walks kRowsPerCta tile rows of one stream (prefetching the next one)
+    const int tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
+    dim3 grid((a.Wstrips + kCtaX - 1) / kCtaX, (tiles_y + kRowsPerCta - 1) / kRowsPerCta, count);
     switch (c->N * 16 + bpt) {
         case 1 * 16 + 4: launch_kernel<1, 4>(a, grid, block, stream); break;
         case 2 * 16 + 2: launch_kernel<2, 2>(a, grid, block, stream); break;
@@ -197,7 +225,7 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
     if (width <= 0 || height <= 0 || width % block || height % block)
         return fail(nullptr, DMSGM_EINVAL, "width/height must be positive multiples of block (R1)");
     if (width % 4) return fail(nullptr, DMSGM_EINVAL, "width must be a multiple of 4");
-    if ((double)(width / block) * (height / block) * 6.0 > 2147483647.0)
+    if ((double)(height / block) * ((width / block + 31) / 32) * 192.0 > 2147483647.0)
         return fail(nullptr, DMSGM_EINVAL, "block grid too large (6*Wb*Hb must be < 2^31)");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -211,7 +239,7 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
     c->W = width; c->H = height; c->N = block;
     c->Wb = width / block; c->Hb = height / block;
     c->S = p->num_streams; c->device = device; c->p = *p;
-    const size_t sbytes = (size_t)c->S * 6 * plane_elems(c) * sizeof(float);
+    const size_t sbytes = (size_t)c->S * stream_floats(c) * sizeof(float);
     for (int i = 0; i < 2; ++i) {
         if ((e = cudaMalloc(&c->state[i], sbytes)) != cudaSuccess ||
             (e = cudaMalloc(&c->fresh[i], (size_t)c->S)) != cudaSuccess) {
@@ -363,8 +391,12 @@ int dmsgm_get_state(dmsgm_ctx* c, int stream, float* out) {
     DeviceGuard g(c->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_get_state sync");
-    const size_t n = 6 * plane_elems(c);
-    e = cudaMemcpy(out, c->state[c->cur] + (size_t)stream * n, n * sizeof(float), cudaMemcpyDeviceToHost);
+    const size_t n = stream_floats(c);
+    float* tmp = (float*)malloc(n * sizeof(float));
+    if (!tmp) return fail(c, DMSGM_ENOMEM, "host allocation failed");
+    e = cudaMemcpy(tmp, c->state[c->cur] + (size_t)stream * n, n * sizeof(float), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) to_public(c, tmp, out);
+    free(tmp);
     if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_get_state copy");
     return DMSGM_OK;
 }
@@ -386,7 +418,12 @@ int dmsgm_set_state(dmsgm_ctx* c, int stream, const float* in) {
     DeviceGuard g(c->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_set_state sync");
-    e = cudaMemcpy(c->state[c->cur] + (size_t)stream * 6 * pe, in, 6 * pe * sizeof(float), cudaMemcpyHostToDevice);
+    const size_t n = stream_floats(c);
+    float* tmp = (float*)malloc(n * sizeof(float));
+    if (!tmp) return fail(c, DMSGM_ENOMEM, "host allocation failed");
+    to_internal(c, in, tmp);
+    e = cudaMemcpy(c->state[c->cur] + (size_t)stream * n, tmp, n * sizeof(float), cudaMemcpyHostToDevice);
+    free(tmp);
     if (e == cudaSuccess) e = cudaMemset(c->fresh[c->cur] + stream, 0, 1);
     if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_set_state copy");
     return DMSGM_OK;
@@ -409,7 +446,7 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     out->width = c->W; out->height = c->H; out->block = c->N;
     out->blocks_x = c->Wb; out->blocks_y = c->Hb; out->num_streams = c->S;
     out->kernels_per_step = 1;
-    out->state_bytes = (size_t)c->S * 6 * plane_elems(c) * sizeof(float);
+    out->state_bytes = (size_t)c->S * stream_floats(c) * sizeof(float);
     // frame read (1 B/px) + mask write (1 B/px) + state read + write (2 x 24 B per block)
     out->algorithmic_bytes_per_frame = 2.0 * c->W * c->H + 2.0 * 24.0 * (double)plane_elems(c);
     return DMSGM_OK;

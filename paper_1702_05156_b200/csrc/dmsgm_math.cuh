@@ -1,10 +1,10 @@
 // dmsgm_math.cuh -- small __host__ __device__ helpers of the DMSGM kernel.
 //
-// Kept host-compilable so the byte-SWAR and cut-point logic can be checked
+// Kept host-compilable so the packed-pixel mask and cut-point logic can be checked
 // exhaustively on the CPU (tests/test_host_math.py builds a tiny host shim).
-// All fp32 arithmetic here is written with explicit round-to-nearest
-// operations so that nvcc never contracts it into FMAs (the kernel is also
-// built with -fmad=false); on the host the shim is built with -ffp-contract=off.
+// fp32 arithmetic here is written with explicit round-to-nearest operations so
+// that nvcc never contracts it into FMAs (the kernel is also built with
+// -fmad=false); on the host the shim is built with -ffp-contract=off.
 #pragma once
 #include <stdint.h>
 
@@ -21,43 +21,37 @@ DM_HD float f_add(float a, float b) { return __fadd_rn(a, b); }
 DM_HD float f_sub(float a, float b) { return __fsub_rn(a, b); }
 DM_HD float f_mul(float a, float b) { return __fmul_rn(a, b); }
 DM_HD float f_div(float a, float b) { return __fdiv_rn(a, b); }
-DM_HD uint32_t byte_sign_spread(uint32_t m) {
-    // PRMT generic mode: selector nibble 8+i replicates the msb of byte i.
+DM_HD float f_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+// PRMT generic mode: result byte i = byte sel_i of {a, b}; selector nibble bit 3
+// replicates the sign (msb) of the selected byte.
+DM_HD uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
-    asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(r) : "r"(m));
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
     return r;
 }
 #else
+#include <math.h>
 DM_HD float f_add(float a, float b) { volatile float r = a + b; return r; }
 DM_HD float f_sub(float a, float b) { volatile float r = a - b; return r; }
 DM_HD float f_mul(float a, float b) { volatile float r = a * b; return r; }
 DM_HD float f_div(float a, float b) { volatile float r = a / b; return r; }
-DM_HD uint32_t byte_sign_spread(uint32_t m) {
+DM_HD float f_fma(float a, float b, float c) { return fmaf(a, b, c); }
+DM_HD uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    const uint64_t x = ((uint64_t)b << 32) | a;
     uint32_t r = 0;
-    for (int i = 0; i < 4; ++i)
-        if (m & (0x80u << (8 * i))) r |= 0xFFu << (8 * i);
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t s = (sel >> (4 * i)) & 0xF;
+        uint32_t byte = (uint32_t)(x >> (8 * (s & 7))) & 0xFF;
+        if (s & 8) byte = (byte & 0x80) ? 0xFF : 0x00;
+        r |= byte << (8 * i);
+    }
     return r;
 }
 #endif
 
-// Per-byte (x - y) mod 256, no borrow across bytes (SWAR subtraction).
-DM_HD uint32_t sub_bytes(uint32_t x, uint32_t y) {
-    return ((x | 0x80808080u) - (y & 0x7F7F7F7Fu)) ^ ((x ^ ~y) & 0x80808080u);
-}
-
-// Per-byte unsigned v > w  ->  0xFF / 0x00.  v > w  <=>  v + (255 - w) carries out of bit 7.
-DM_HD uint32_t gt_bytes(uint32_t v, uint32_t w) {
-    const uint32_t k = ~w;
-    const uint32_t s = (v & 0x7F7F7F7Fu) + (k & 0x7F7F7F7Fu);   // bit 7 = carry into bit 7
-    const uint32_t maj = (v & k) | ((v | k) & s);                // carry out of bit 7 (in bit 7)
-    return byte_sign_spread(maj);
-}
-
-// Mask of four pixels against per-byte background intervals [a, a+w] (w >= 0),
-// with per-byte "all foreground" override f (0xFF bytes): 255 = foreground.
-DM_HD uint32_t mask_bytes(uint32_t px, uint32_t a, uint32_t w, uint32_t f) {
-    return gt_bytes(sub_bytes(px, a), w) | f;
-}
+// Bytes {0,1} / {2,3} of a pixel word as two 16-bit lanes (zero-extended).
+DM_HD uint32_t lanes_lo(uint32_t w) { return prmt(w, 0, 0x4140); }
+DM_HD uint32_t lanes_hi(uint32_t w) { return prmt(w, 0, 0x4342); }
 
 // Literal per-pixel classification predicate of App. E P:657 with reading R14:
 // foreground iff fl(fl(I - mu)^2) > T.
@@ -68,13 +62,12 @@ DM_HD bool fg_pred(float I, float mu, float T) {
 
 // Background interval of the classification for integer intensities.
 // {I in Z : !fg_pred(I, mu, T)} is an interval [a, b] (fl(I-mu) is monotone in I and
-// fl(x*x) is monotone in |x|).  Returns it clamped to [0,255] as (a, w = b - a) and
-// `empty` when no intensity in [0,255] is background.  The estimate floor(mu +/- r),
-// r ~ sqrt(T), is refined by testing the literal predicate at est-1, est, est+1.
+// fl(x*x) is monotone in |x|).  Returned clamped to [0,255]; a = 256 when no intensity
+// in [0,255] is background.  The estimate floor(mu +/- r), r ~ sqrt(T), is refined by
+// testing the literal predicate at est-1, est, est+1 (SURVEY pin P13, host-tested).
 struct Interval {
     int a;
-    int w;
-    bool empty;
+    int b;
 };
 
 DM_HD Interval bg_interval(float mu, float T, float r) {
@@ -87,8 +80,8 @@ DM_HD Interval bg_interval(float mu, float T, float r) {
     const int hi = __float2int_rd(hi_f);
     const int lo = __float2int_ru(lo_f);
 #else
-    const int hi = (int)__builtin_floorf(hi_f);
-    const int lo = (int)__builtin_ceilf(lo_f);
+    const int hi = (int)floorf(hi_f);
+    const int lo = (int)ceilf(lo_f);
 #endif
     // upper end: the largest k in {hi+1, hi, hi-1} that is background
     const bool p_h1 = fg_pred((float)(hi + 1), mu, T);
@@ -98,17 +91,30 @@ DM_HD Interval bg_interval(float mu, float T, float r) {
     const bool p_lm = fg_pred((float)(lo - 1), mu, T);
     const bool p_l0 = fg_pred((float)lo, mu, T);
     const bool p_l1 = fg_pred((float)(lo + 1), mu, T);
-    const bool none_hi = p_h1 && p_h0 && p_hm;
-    const bool none_lo = p_lm && p_l0 && p_l1;
+    const bool none = (p_h1 && p_h0 && p_hm) || (p_lm && p_l0 && p_l1);
     int b = !p_h1 ? hi + 1 : (!p_h0 ? hi : hi - 1);
     int a = !p_lm ? lo - 1 : (!p_l0 ? lo : lo + 1);
     a = a < 0 ? 0 : a;
     b = b > 255 ? 255 : b;
     Interval iv;
-    iv.empty = none_hi || none_lo || a > b;
-    iv.a = iv.empty ? 0 : a;
-    iv.w = iv.empty ? 0 : b - a;
+    iv.a = (none || a > b) ? 256 : a;
+    iv.b = b < 0 ? 0 : b;
     return iv;
+}
+
+// Per-16-bit-lane keys of an interval: x = lane + (0x8000 - a) has bit 15 set iff
+// lane >= a; y = (0x8000 + b) - lane has bit 15 set iff lane <= b (lanes <= 255, so no
+// carry/borrow crosses a lane).  a = 256 makes x's bit 15 always clear (all foreground).
+DM_HD uint32_t key_a(int a) { return (uint32_t)(0x8000 - a); }
+DM_HD uint32_t key_b(int b) { return (uint32_t)(0x8000 + b); }
+
+// Mask of four pixels given as two 16-bit-lane words (lanes_lo / lanes_hi) and the
+// packed keys of each lane's block: 0xFF = foreground (outside [a, b]).
+DM_HD uint32_t mask_word(uint32_t lo, uint32_t hi, uint32_t ka_lo, uint32_t kb_lo, uint32_t ka_hi,
+                         uint32_t kb_hi) {
+    const uint32_t fl = ~((lo + ka_lo) & (kb_lo - lo));   // bit 15 / 31: pixel 0 / 1 foreground
+    const uint32_t fh = ~((hi + ka_hi) & (kb_hi - hi));   // bit 15 / 31: pixel 2 / 3 foreground
+    return prmt(fl, fh, 0xFDB9);                          // sign-spread bytes 1,3 of fl, fh
 }
 
 }  // namespace dmsgm

@@ -12,12 +12,11 @@ using namespace dmsgm;
 
 static int check_interval(float mu, float T, float r, long long* fails) {
     const Interval iv = bg_interval(mu, T, r);
+    const uint32_t ka = key_a(iv.a) * 0x00010001u, kb = key_b(iv.b) * 0x00010001u;
     uint8_t got[256];
     for (int I = 0; I < 256; I += 4) {
         uint32_t px = (uint32_t)I | ((uint32_t)(I + 1) << 8) | ((uint32_t)(I + 2) << 16) | ((uint32_t)(I + 3) << 24);
-        uint32_t a4 = (uint32_t)iv.a * 0x01010101u, w4 = (uint32_t)iv.w * 0x01010101u;
-        uint32_t f4 = iv.empty ? 0xFFFFFFFFu : 0u;
-        uint32_t m = mask_bytes(px, a4, w4, f4);
+        uint32_t m = mask_word(lanes_lo(px), lanes_hi(px), ka, kb, ka, kb);
         for (int j = 0; j < 4; ++j) got[I + j] = (m >> (8 * j)) & 0xFF;
     }
     int bad = 0;
@@ -27,8 +26,7 @@ static int check_interval(float mu, float T, float r, long long* fails) {
     }
     if (bad) {
         if (*fails < 10)
-            printf("MISMATCH mu=%.9g T=%.9g r=%.9g a=%d w=%d empty=%d bad=%d\n", mu, T, r, iv.a, iv.w,
-                   (int)iv.empty, bad);
+            printf("MISMATCH mu=%.9g T=%.9g r=%.9g a=%d b=%d bad=%d\n", mu, T, r, iv.a, iv.b, bad);
         ++*fails;
     }
     return bad;
@@ -37,19 +35,30 @@ static int check_interval(float mu, float T, float r, long long* fails) {
 int main(int argc, char** argv) {
     long long trials = argc > 1 ? atoll(argv[1]) : 2000000;
     long long fails = 0;
-    // 1) SWAR primitives, every byte pair in every lane
+    // 1) lane primitives: every (pixel, a, b) in every byte position, mixed per-lane keys
     std::mt19937 rng(1234);
     long long swar_bad = 0;
-    for (int x = 0; x < 256; ++x)
-        for (int y = 0; y < 256; ++y)
-            for (int lane = 0; lane < 4; ++lane) {
-                uint32_t X = rng(), Y = rng();
-                X = (X & ~(0xFFu << (8 * lane))) | ((uint32_t)x << (8 * lane));
-                Y = (Y & ~(0xFFu << (8 * lane))) | ((uint32_t)y << (8 * lane));
-                uint32_t d = (sub_bytes(X, Y) >> (8 * lane)) & 0xFF;
-                uint32_t g = (gt_bytes(X, Y) >> (8 * lane)) & 0xFF;
-                if (d != (uint32_t)((x - y) & 0xFF)) ++swar_bad;
-                if (g != (x > y ? 0xFFu : 0u)) ++swar_bad;
+    for (int a = 0; a <= 256; ++a)
+        for (int b = 0; b < 256; b += (a == 256 ? 255 : 1))
+            for (int pos = 0; pos < 4; ++pos) {
+                const int I = (int)(rng() & 0xFF);
+                uint32_t px = rng();
+                px = (px & ~(0xFFu << (8 * pos))) | ((uint32_t)I << (8 * pos));
+                // lane of byte pos gets keys (a, b); other lanes get random keys
+                uint32_t ka[2], kb[2];
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t k0 = key_a((int)(rng() % 257)), k1 = key_a((int)(rng() % 257));
+                    uint32_t m0 = key_b((int)(rng() % 256)), m1 = key_b((int)(rng() % 256));
+                    ka[h] = k0 | (k1 << 16);
+                    kb[h] = m0 | (m1 << 16);
+                }
+                const int h = pos / 2, l = pos % 2;
+                ka[h] = (ka[h] & ~(0xFFFFu << (16 * l))) | (key_a(a) << (16 * l));
+                kb[h] = (kb[h] & ~(0xFFFFu << (16 * l))) | (key_b(b) << (16 * l));
+                const uint32_t m = mask_word(lanes_lo(px), lanes_hi(px), ka[0], kb[0], ka[1], kb[1]);
+                const uint32_t got = (m >> (8 * pos)) & 0xFF;
+                const uint32_t expect = (a <= 255 && I >= a && I <= b) ? 0u : 0xFFu;
+                if (got != expect) ++swar_bad;
             }
     printf("swar_bad %lld\n", swar_bad);
 
