@@ -53,8 +53,39 @@ struct dmsgm_ctx {
     cudaStream_t pipe[kPipeStreams];
     cudaEvent_t ev_start;
     bool pipe_ready;
+    int staged;        // 1: persistent smem-staged kernel (N = 4 with even Wb, N = 8)
+    int staged_ctas;   // resident CTAs of the staged kernel on this device
     char err[512];
 };
+
+// Persistent staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
+template <int N, int BPT>
+cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, int count, cudaStream_t stream) {
+    StagedArgs sa;
+    sa.tiles_xc = (a.Wstrips + kCtaX - 1) / kCtaX;
+    sa.tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
+    sa.items = count * sa.tiles_xc * sa.tiles_y;
+    sa.width = c->W;
+    sa.height = c->H;
+    const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
+    dmsgm_step_staged<N, BPT><<<grid, dim3(kCtaX, kCtaY, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(a, sa);
+    return cudaGetLastError();
+}
+
+template <int N, int BPT>
+cudaError_t setup_staged(dmsgm_ctx* c) {
+    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Staged<N, BPT>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT>, kCtaX * kCtaY,
+                                                      Staged<N, BPT>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    if (e != cudaSuccess) return e;
+    c->staged_ctas = (per_sm > 0 ? per_sm : 1) * sms;
+    return cudaSuccess;
+}
 
 namespace {
 
@@ -104,6 +135,8 @@ KParams kparams(const dmsgm_params& p) {
     k.f_m = p.var_floor_match; k.f_c = p.var_floor_classify;
     k.lambda = p.decay_lambda; k.theta_v = p.decay_var_thresh;
     k.update_rule = p.update_rule; k.classify_rule = p.classify_rule;
+    const float tmin = p.theta_d * p.var_floor_classify;   // the kernel's fp32 product
+    k.interval_may_be_empty = (tmin >= 0.25f) ? 0 : 1;
     return k;
 }
 
@@ -176,6 +209,10 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     // each CTA walks kRowsPerCta tile rows of one stream (prefetching the next one)
     const int tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
     dim3 grid((a.Wstrips + kCtaX - 1) / kCtaX, (tiles_y + kRowsPerCta - 1) / kRowsPerCta, count);
+    if (c->staged) {
+        if (c->N == 4 && bpt == 2) return launch_staged<4, 2>(c, a, count, stream);
+        if (c->N == 8) return launch_staged<8, 1>(c, a, count, stream);
+    }
     switch (c->N * 16 + bpt) {
         case 1 * 16 + 4: launch_kernel<1, 4>(a, grid, block, stream); break;
         case 2 * 16 + 2: launch_kernel<2, 2>(a, grid, block, stream); break;
@@ -245,6 +282,19 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
             (e = cudaMalloc(&c->fresh[i], (size_t)c->S)) != cudaSuccess) {
             dmsgm_destroy(c);
             return fail(nullptr, DMSGM_ENOMEM, "cudaMalloc of %zu B failed: %s", sbytes, cudaGetErrorString(e));
+        }
+    }
+    {
+        const char* kenv = getenv("DMSGM_KERNEL");           // "generic" forces the register-path kernel
+        const bool want = !(kenv && strcmp(kenv, "generic") == 0);
+        c->staged = 0;
+        if (want && ((block == 4 && c->Wb % 2 == 0) || block == 8)) {
+            e = block == 4 ? setup_staged<4, 2>(c) : setup_staged<8, 1>(c);
+            if (e != cudaSuccess) {
+                dmsgm_destroy(c);
+                return fail(nullptr, DMSGM_ECUDA, "staged kernel setup: %s", cudaGetErrorString(e));
+            }
+            c->staged = 1;
         }
     }
     if ((e = cudaMemset(c->state[0], 0, sbytes)) != cudaSuccess ||

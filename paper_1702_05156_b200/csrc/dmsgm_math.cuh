@@ -70,28 +70,29 @@ struct Interval {
     int b;
 };
 
-DM_HD Interval bg_interval(float mu, float T, float r) {
+DM_HD Interval bg_interval(float mu, float T, float r, bool may_be_empty = true) {
     // r: any estimate of sqrt(T) with relative error << 1/512 (caller supplies it).
+    // may_be_empty = false is allowed when T >= 0.25 is guaranteed: the integer nearest
+    // to mu then has fl(d*d) <= 0.25 <= T, so the interval is never empty.
     float hi_f = f_add(mu, r);
     float lo_f = f_sub(mu, r);
     hi_f = hi_f < -2.0f ? -2.0f : (hi_f > 257.0f ? 257.0f : hi_f);
     lo_f = lo_f < -2.0f ? -2.0f : (lo_f > 257.0f ? 257.0f : lo_f);
-#if defined(__CUDA_ARCH__)
-    const int hi = __float2int_rd(hi_f);
-    const int lo = __float2int_ru(lo_f);
-#else
-    const int hi = (int)floorf(hi_f);
-    const int lo = (int)ceilf(lo_f);
-#endif
+    const float hf = floorf(hi_f);          // candidates are small integers: exact in fp32
+    const float lf = ceilf(lo_f);
     // upper end: the largest k in {hi+1, hi, hi-1} that is background
-    const bool p_h1 = fg_pred((float)(hi + 1), mu, T);
-    const bool p_h0 = fg_pred((float)hi, mu, T);
-    const bool p_hm = fg_pred((float)(hi - 1), mu, T);
+    const bool p_h1 = fg_pred(f_add(hf, 1.0f), mu, T);
+    const bool p_h0 = fg_pred(hf, mu, T);
     // lower end: the smallest k in {lo-1, lo, lo+1} that is background
-    const bool p_lm = fg_pred((float)(lo - 1), mu, T);
-    const bool p_l0 = fg_pred((float)lo, mu, T);
-    const bool p_l1 = fg_pred((float)(lo + 1), mu, T);
-    const bool none = (p_h1 && p_h0 && p_hm) || (p_lm && p_l0 && p_l1);
+    const bool p_lm = fg_pred(f_sub(lf, 1.0f), mu, T);
+    const bool p_l0 = fg_pred(lf, mu, T);
+    bool none = false;
+    if (may_be_empty) {
+        const bool p_hm = fg_pred(f_sub(hf, 1.0f), mu, T);
+        const bool p_l1 = fg_pred(f_add(lf, 1.0f), mu, T);
+        none = (p_h1 && p_h0 && p_hm) || (p_lm && p_l0 && p_l1);
+    }
+    const int hi = (int)hf, lo = (int)lf;
     int b = !p_h1 ? hi + 1 : (!p_h0 ? hi : hi - 1);
     int a = !p_lm ? lo - 1 : (!p_l0 ? lo : lo + 1);
     a = a < 0 ? 0 : a;

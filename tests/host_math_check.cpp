@@ -11,7 +11,8 @@
 using namespace dmsgm;
 
 static int check_interval(float mu, float T, float r, long long* fails) {
-    const Interval iv = bg_interval(mu, T, r);
+    // the short form (no emptiness tests) is used by the kernel only when T >= 0.25
+    const Interval iv = bg_interval(mu, T, r, !(T >= 0.25f));
     const uint32_t ka = key_a(iv.a) * 0x00010001u, kb = key_b(iv.b) * 0x00010001u;
     uint8_t got[256];
     for (int I = 0; I < 256; I += 4) {
@@ -96,6 +97,10 @@ int main(int argc, char** argv) {
         const float sq = sqrtf(T);
         const float r = sq * (1.0f + (U(rng) - 0.5f) * 4e-6f);
         check_interval(mu, T, r, &fails);
+        if (T >= 0.25f) {   // the full form must agree too
+            const Interval a1 = bg_interval(mu, T, r, true), a2 = bg_interval(mu, T, r, false);
+            if (a1.a != a2.a || (a1.a <= 255 && a1.b != a2.b)) ++fails;
+        }
     }
     printf("interval_fails %lld of %lld\n", fails, trials);
     return (swar_bad || fails) ? 1 : 0;

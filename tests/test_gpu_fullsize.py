@@ -15,7 +15,8 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
 @pytest.mark.parametrize("name,T,sample", [("C4", 3, [0, 17, 31]), ("C5", 2, [5, 63])])
-def test_fullsize_sampled_streams(cuda_lib, oracle_mod, name, T, sample):
+def test_fullsize_sampled_streams(cuda_lib, oracle_mod, name, T, sample, monkeypatch):
+    monkeypatch.delenv("DMSGM_KERNEL", raising=False)       # the bench's kernel
     import torch
     dm = cuda_lib
     cfg = synth.config(name, T=T)

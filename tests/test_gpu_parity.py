@@ -20,6 +20,17 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 IDENT = np.eye(3).reshape(9)
 
 
+@pytest.fixture(params=["default", "generic"])
+def kernel_path(request, monkeypatch):
+    """default: the persistent shared-memory-staged kernel where it applies (N = 4 with
+    even Wb, N = 8); generic: force the register-path kernel (DMSGM_KERNEL=generic)."""
+    if request.param == "generic":
+        monkeypatch.setenv("DMSGM_KERNEL", "generic")
+    else:
+        monkeypatch.delenv("DMSGM_KERNEL", raising=False)
+    return request.param
+
+
 def _check_run(dm, oracle_mod, frames, Hs, N, pg, po, init=None, mode="step", bitwise=False,
                snapshot_every=1):
     gm, gs = run_gpu(dm, frames, Hs, N, pg, init, mode=mode, snapshot_every=snapshot_every)
@@ -65,7 +76,7 @@ def test_hand_worked_gpu(cuda_lib, oracle_mod, case):
 
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("name,T", [("C1", 10), ("C2", 60), ("C3", 40)])
-def test_sequence_parity(cuda_lib, oracle_mod, name, T):
+def test_sequence_parity(cuda_lib, oracle_mod, name, T, kernel_path):
     cfg = synth.config(name, T=T)
     seq = synth.generate(cfg)
     pg, po = params_pair(cuda_lib, oracle_mod, cfg.S)
@@ -86,7 +97,7 @@ def test_sequence_parity_bitwise_no_decay(cuda_lib, oracle_mod, name, T):
 @pytest.mark.parametrize("N,W,H,S", [(1, 100, 20, 2), (2, 72, 30, 2), (4, 200, 52, 3), (4, 1000, 36, 1),
                                      (8, 264, 104, 2), (16, 272, 80, 2), (4, 4, 4, 1), (8, 8, 8, 3)])
 @pytest.mark.parametrize("variant", ["default", "decay_often", "no_decay", "appendix_rules"])
-def test_random_state_parity(cuda_lib, oracle_mod, N, W, H, S, variant):
+def test_random_state_parity(cuda_lib, oracle_mod, N, W, H, S, variant, kernel_path):
     rng = np.random.default_rng(1000 * N + W + H + S + len(variant))
     kw = {"default": {}, "decay_often": dict(decay_var_thresh=100.0, decay_lambda=0.01),
           "no_decay": dict(decay_lambda=0.0),
@@ -113,7 +124,7 @@ def test_random_state_parity(cuda_lib, oracle_mod, N, W, H, S, variant):
     _check_run(cuda_lib, oracle_mod, frames, Hs, N, pg, po, init=init, bitwise=bitwise)
 
 
-def test_exposure_parity(cuda_lib, oracle_mod):
+def test_exposure_parity(cuda_lib, oracle_mod, kernel_path):
     """Large motions, w <= 0 and far-out projections: exposed blocks reset identically."""
     rng = np.random.default_rng(5)
     N, W, H, S = 4, 64, 32, 4
@@ -139,7 +150,7 @@ def test_step_n_equals_oracle(cuda_lib, oracle_mod, T):
     _check_run(cuda_lib, oracle_mod, seq.frames, seq.homographies, cfg.N, pg, po, mode="step_n")
 
 
-def test_step_host_equals_oracle(cuda_lib, oracle_mod):
+def test_step_host_equals_oracle(cuda_lib, oracle_mod, kernel_path):
     cfg = synth.config("C4", W=320, H=240, T=5, S=11)
     seq = synth.generate(cfg)
     pg, po = params_pair(cuda_lib, oracle_mod, 11)
