@@ -4,6 +4,8 @@
 // [S][6][Hb][Wb]) and per-stream fresh flags (two ping-pong arrays [S]); launches
 // the fused step kernel (dmsgm_kernel.cuh) once per frame batch; captures T-step
 // batches into CUDA graphs; pipelines host<->device copies for dmsgm_step_host.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
@@ -53,22 +55,69 @@ struct dmsgm_ctx {
     cudaStream_t pipe[kPipeStreams];
     cudaEvent_t ev_start;
     bool pipe_ready;
-    int staged;        // 1: persistent smem-staged kernel (N = 4 with even Wb, N = 8)
+    int staged;        // 1: persistent TMA-staged kernel (N = 4 with even Wb, N = 8)
     int staged_ctas;   // resident CTAs of the staged kernel on this device
+    CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (chunk-SoA, 4-D)
     char err[512];
 };
 
-// Persistent staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// 4-D view of a state buffer: {24 floats of a chunk, chunks per row, block rows, streams}.
+bool encode_state_map(const dmsgm_ctx* c, float* base, int xc, int wrows, CUtensorMap* out) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const int tx = (c->Wb + kTile - 1) / kTile;
+    cuuint64_t dims[4] = {(cuuint64_t)kTileFloats, (cuuint64_t)tx, (cuuint64_t)c->Hb, (cuuint64_t)c->S};
+    cuuint64_t strides[3] = {(cuuint64_t)kTileFloats * 4, (cuuint64_t)tx * kTileFloats * 4,
+                             (cuuint64_t)c->Hb * tx * kTileFloats * 4};
+    cuuint32_t box[4] = {(cuuint32_t)kTileFloats, (cuuint32_t)xc, (cuuint32_t)wrows, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 3-D view of a frame batch: {width bytes, rows, streams}; box 256 B x rows x 1.
+bool encode_frame_map(const dmsgm_ctx* c, const uint8_t* base, size_t pitch, int count, int box_rows,
+                      CUtensorMap* out) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)c->W, (cuuint64_t)c->H, (cuuint64_t)count};
+    cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * c->H};
+    cuuint32_t box[3] = {256, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+// Persistent TMA-staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
 template <int N, int BPT>
-cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, int count, cudaStream_t stream) {
+cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames, size_t fpitch, int s0,
+                          int count, int parity, cudaStream_t stream) {
     StagedArgs sa;
     sa.tiles_xc = (a.Wstrips + kCtaX - 1) / kCtaX;
     sa.tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
     sa.items = count * sa.tiles_xc * sa.tiles_y;
-    sa.width = c->W;
-    sa.height = c->H;
+    sa.s0 = s0;
+    CUtensorMap fmap;
+    if (!encode_frame_map(c, frames, fpitch, count, N * kCtaY, &fmap)) return cudaErrorInvalidValue;
     const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
-    dmsgm_step_staged<N, BPT><<<grid, dim3(kCtaX, kCtaY, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(a, sa);
+    dmsgm_step_staged<N, BPT><<<grid, dim3(kCtaX, kCtaY, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(
+        a, sa, fmap, c->state_map[parity]);
     return cudaGetLastError();
 }
 
@@ -84,6 +133,9 @@ cudaError_t setup_staged(dmsgm_ctx* c) {
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     if (e != cudaSuccess) return e;
     c->staged_ctas = (per_sm > 0 ? per_sm : 1) * sms;
+    for (int i = 0; i < 2; ++i)
+        if (!encode_state_map(c, c->state[i], Staged<N, BPT>::XC, Staged<N, BPT>::WROWS, &c->state_map[i]))
+            return cudaErrorInvalidValue;
     return cudaSuccess;
 }
 
@@ -210,8 +262,8 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     const int tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
     dim3 grid((a.Wstrips + kCtaX - 1) / kCtaX, (tiles_y + kRowsPerCta - 1) / kRowsPerCta, count);
     if (c->staged) {
-        if (c->N == 4 && bpt == 2) return launch_staged<4, 2>(c, a, count, stream);
-        if (c->N == 8) return launch_staged<8, 1>(c, a, count, stream);
+        if (c->N == 4 && bpt == 2) return launch_staged<4, 2>(c, a, frames, fpitch, s0, count, parity, stream);
+        if (c->N == 8) return launch_staged<8, 1>(c, a, frames, fpitch, s0, count, parity, stream);
     }
     switch (c->N * 16 + bpt) {
         case 1 * 16 + 4: launch_kernel<1, 4>(a, grid, block, stream); break;

@@ -14,6 +14,6 @@ cat $OUT/bench_$TAG.json
 timeout 900 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $OUT/launches_$TAG.csv python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu-baseline \
   > $OUT/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:dmsgm_step_kernel -s 8 -c 2 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:dmsgm_step -s 8 -c 2 \
   -o $OUT/prof_$TAG -f python bench.py --steps 6 --warmup 5 --no-e2e --no-cpu-baseline \
   > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"

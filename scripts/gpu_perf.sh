@@ -14,7 +14,7 @@ for cfg in ${CONFIGS:-C4}; do
   python -c "import json,sys; b=json.loads(open('$OUT/bench_${TAG}_$cfg.json').read().strip().splitlines()[-1]); print('$cfg', round(b['value']), b['unit'], 'ms/step', round(b['ms_per_step'],4), 'GB/s', round(b['roofline']['achieved']), 'frac', round(b['roofline']['frac'],3), 'clk', b['clocks']['sm_mhz'])"
 done
 if [ "${NCU:-1}" = "1" ]; then
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:dmsgm_step_kernel -s 8 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:dmsgm_step -s 8 -c 1 \
   -o $OUT/prof_$TAG -f python bench.py --steps 4 --warmup 5 --no-e2e --no-cpu-baseline \
   > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 fi
