@@ -55,8 +55,9 @@ struct dmsgm_ctx {
     cudaStream_t pipe[kPipeStreams];
     cudaEvent_t ev_start;
     bool pipe_ready;
-    int staged;        // 1: persistent TMA-staged kernel (N = 4 with even Wb, N = 8)
+    int staged;        // 1: persistent TMA-staged kernel (N = 4, N = 8)
     int staged_ctas;   // resident CTAs of the staged kernel on this device
+    int staged_occ;    // register-capped occupancy variant (3 or 4 CTAs/SM)
     CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (chunk-SoA, 4-D)
     char err[512];
 };
@@ -105,29 +106,29 @@ bool encode_frame_map(const dmsgm_ctx* c, const uint8_t* base, size_t pitch, int
 }  // namespace
 
 // Persistent TMA-staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
-template <int N, int BPT>
+template <int N, int BPT, int MINB>
 cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames, size_t fpitch, int s0,
                           int count, int parity, cudaStream_t stream) {
     StagedArgs sa;
-    sa.tiles_xc = (a.Wstrips + kCtaX - 1) / kCtaX;
+    sa.tiles_xc = (c->Wb + Staged<N, BPT>::TWB - 1) / Staged<N, BPT>::TWB;
     sa.tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
     sa.items = count * sa.tiles_xc * sa.tiles_y;
     sa.s0 = s0;
     CUtensorMap fmap;
     if (!encode_frame_map(c, frames, fpitch, count, N * kCtaY, &fmap)) return cudaErrorInvalidValue;
     const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
-    dmsgm_step_staged<N, BPT><<<grid, dim3(kCtaX, kCtaY, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(
+    dmsgm_step_staged<N, BPT, MINB><<<grid, dim3(kCtaX, kCtaY, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(
         a, sa, fmap, c->state_map[parity]);
     return cudaGetLastError();
 }
 
-template <int N, int BPT>
+template <int N, int BPT, int MINB>
 cudaError_t setup_staged(dmsgm_ctx* c) {
-    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Staged<N, BPT>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT>, kCtaX * kCtaY,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB>, kCtaX * kCtaY,
                                                       Staged<N, BPT>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -262,8 +263,13 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     const int tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
     dim3 grid((a.Wstrips + kCtaX - 1) / kCtaX, (tiles_y + kRowsPerCta - 1) / kRowsPerCta, count);
     if (c->staged) {
-        if (c->N == 4 && bpt == 2) return launch_staged<4, 2>(c, a, frames, fpitch, s0, count, parity, stream);
-        if (c->N == 8) return launch_staged<8, 1>(c, a, frames, fpitch, s0, count, parity, stream);
+        const bool o3 = c->staged_occ == 3;
+        if (c->N == 4)
+            return o3 ? launch_staged<4, 2, 3>(c, a, frames, fpitch, s0, count, parity, stream)
+                      : launch_staged<4, 2, 4>(c, a, frames, fpitch, s0, count, parity, stream);
+        if (c->N == 8)
+            return o3 ? launch_staged<8, 1, 3>(c, a, frames, fpitch, s0, count, parity, stream)
+                      : launch_staged<8, 1, 4>(c, a, frames, fpitch, s0, count, parity, stream);
     }
     switch (c->N * 16 + bpt) {
         case 1 * 16 + 4: launch_kernel<1, 4>(a, grid, block, stream); break;
@@ -340,8 +346,11 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
         const char* kenv = getenv("DMSGM_KERNEL");           // "generic" forces the register-path kernel
         const bool want = !(kenv && strcmp(kenv, "generic") == 0);
         c->staged = 0;
-        if (want && ((block == 4 && c->Wb % 2 == 0) || block == 8)) {
-            e = block == 4 ? setup_staged<4, 2>(c) : setup_staged<8, 1>(c);
+        if (want && (block == 4 || block == 8)) {
+            const char* oenv = getenv("DMSGM_STAGED_OCC");   // 3 or 4 resident CTAs per SM (register cap)
+            c->staged_occ = (oenv && atoi(oenv) == 3) ? 3 : 4;
+            if (c->staged_occ == 3) e = block == 4 ? setup_staged<4, 2, 3>(c) : setup_staged<8, 1, 3>(c);
+            else e = block == 4 ? setup_staged<4, 2, 4>(c) : setup_staged<8, 1, 4>(c);
             if (e != cudaSuccess) {
                 dmsgm_destroy(c);
                 return fail(nullptr, DMSGM_ECUDA, "staged kernel setup: %s", cudaGetErrorString(e));
