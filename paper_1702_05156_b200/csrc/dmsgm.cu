@@ -106,7 +106,7 @@ bool encode_frame_map(const dmsgm_ctx* c, const uint8_t* base, size_t pitch, int
 }  // namespace
 
 // Persistent TMA-staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
-template <int N, int BPT, int MINB>
+template <int N, int BPT, int MINB, bool RULES>
 cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames, size_t fpitch, int s0,
                           int count, int parity, cudaStream_t stream) {
     StagedArgs sa;
@@ -117,18 +117,21 @@ cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames
     CUtensorMap fmap;
     if (!encode_frame_map(c, frames, fpitch, count, N * kCtaY, &fmap)) return cudaErrorInvalidValue;
     const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
-    dmsgm_step_staged<N, BPT, MINB><<<grid, dim3(kCtaX, kCtaY, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(
+    dmsgm_step_staged<N, BPT, MINB, RULES><<<grid, dim3(kCtaX, kCtaY, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(
         a, sa, fmap, c->state_map[parity]);
     return cudaGetLastError();
 }
 
 template <int N, int BPT, int MINB>
 cudaError_t setup_staged(dmsgm_ctx* c) {
-    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Staged<N, BPT>::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT>::SMEM_BYTES);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Staged<N, BPT>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB>, kCtaX * kCtaY,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB, false>, kCtaX * kCtaY,
                                                       Staged<N, BPT>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -263,13 +266,22 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     const int tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
     dim3 grid((a.Wstrips + kCtaX - 1) / kCtaX, (tiles_y + kRowsPerCta - 1) / kRowsPerCta, count);
     if (c->staged) {
+        // RULES = the App. E compatibility switches (R27/R28) are on: runtime-switched code;
+        // otherwise the default rules are compiled in without branches.
+        const bool rules = c->p.update_rule != 0 || c->p.classify_rule != 0;
         const bool o3 = c->staged_occ == 3;
-        if (c->N == 4)
-            return o3 ? launch_staged<4, 2, 3>(c, a, frames, fpitch, s0, count, parity, stream)
-                      : launch_staged<4, 2, 4>(c, a, frames, fpitch, s0, count, parity, stream);
-        if (c->N == 8)
-            return o3 ? launch_staged<8, 1, 3>(c, a, frames, fpitch, s0, count, parity, stream)
-                      : launch_staged<8, 1, 4>(c, a, frames, fpitch, s0, count, parity, stream);
+#define DMSGM_STAGED(NN, BB, OO)                                                                   \
+    return rules ? launch_staged<NN, BB, OO, true>(c, a, frames, fpitch, s0, count, parity, stream) \
+                 : launch_staged<NN, BB, OO, false>(c, a, frames, fpitch, s0, count, parity, stream)
+        if (c->N == 4) {
+            if (o3) DMSGM_STAGED(4, 2, 3);
+            DMSGM_STAGED(4, 2, 4);
+        }
+        if (c->N == 8) {
+            if (o3) DMSGM_STAGED(8, 1, 3);
+            DMSGM_STAGED(8, 1, 4);
+        }
+#undef DMSGM_STAGED
     }
     switch (c->N * 16 + bpt) {
         case 1 * 16 + 4: launch_kernel<1, 4>(a, grid, block, stream); break;
