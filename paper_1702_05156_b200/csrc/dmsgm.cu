@@ -117,7 +117,7 @@ cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames
     CUtensorMap fmap;
     if (!encode_frame_map(c, frames, fpitch, count, N * kCtaY, &fmap)) return cudaErrorInvalidValue;
     const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
-    dmsgm_step_staged<N, BPT, MINB, RULES><<<grid, dim3(kCtaX, kCtaY, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(
+    dmsgm_step_staged<N, BPT, MINB, RULES><<<grid, dim3(kCtaX, kCtaY + 1, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(
         a, sa, fmap, c->state_map[parity]);
     return cudaGetLastError();
 }
@@ -131,8 +131,8 @@ cudaError_t setup_staged(dmsgm_ctx* c) {
                                  Staged<N, BPT>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB, false>, kCtaX * kCtaY,
-                                                      Staged<N, BPT>::SMEM_BYTES);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB, false>,
+                                                      kStagedThreads, Staged<N, BPT>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     if (e != cudaSuccess) return e;
@@ -360,7 +360,7 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
         c->staged = 0;
         if (want && (block == 4 || block == 8)) {
             const char* oenv = getenv("DMSGM_STAGED_OCC");   // 3 or 4 resident CTAs per SM (register cap)
-            c->staged_occ = (oenv && atoi(oenv) == 3) ? 3 : 4;
+            c->staged_occ = (oenv && atoi(oenv) == 4) ? 4 : 3;
             if (c->staged_occ == 3) e = block == 4 ? setup_staged<4, 2, 3>(c) : setup_staged<8, 1, 3>(c);
             else e = block == 4 ? setup_staged<4, 2, 4>(c) : setup_staged<8, 1, 4>(c);
             if (e != cudaSuccess) {
