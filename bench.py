@@ -334,6 +334,7 @@ def run_dmsgm(args, rank, world, local):
                          f"{wall:.1f} s wall, one single-threaded oracle step per stream per thread"}
 
     clocks = sampler.summary()
+    kernel_name = info.kernel.decode()
     ctx.close()
     if rank == 0:
         traffic = ncu_traffic(args.config)
@@ -352,7 +353,7 @@ def run_dmsgm(args, rank, world, local):
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_step,
                          "peak_source": peak_src,
-                         "kernel": f"dmsgm_step_kernel<{N}> (1 launch/step)"},
+                         "kernel": f"{kernel_name} (1 launch/step)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": info.kernels_per_step * args.steps,

@@ -71,8 +71,9 @@ typedef struct {
     int blocks_x, blocks_y;        /* Wb = W/N, Hb = H/N                        */
     int num_streams;               /* S                                         */
     int kernels_per_step;          /* kernel launches per dmsgm_step (1)       */
-    size_t state_bytes;            /* one state buffer: S*6*Hb*Wb*4            */
+    size_t state_bytes;            /* one state buffer (internal chunk-SoA layout, padded to Wb%4) */
     double algorithmic_bytes_per_frame; /* frame read + mask write + state read+write, one stream */
+    char kernel[64];               /* the kernel dmsgm_step launches, e.g. "dmsgm_step_staged<4,2>" */
 } dmsgm_info;
 
 /* Create a context on CUDA device `device` (W, H in pixels, N = block).  Allocates two

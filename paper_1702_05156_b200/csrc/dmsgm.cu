@@ -572,6 +572,11 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     out->state_bytes = (size_t)c->S * stream_floats(c) * sizeof(float);
     // frame read (1 B/px) + mask write (1 B/px) + state read + write (2 x 24 B per block)
     out->algorithmic_bytes_per_frame = 2.0 * c->W * c->H + 2.0 * 24.0 * (double)plane_elems(c);
+    if (c->staged)
+        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d> (TMA, persistent)", c->N,
+                 c->N == 4 ? 2 : 1, c->staged_occ);
+    else
+        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_kernel<%d,%d>", c->N, bpt_of(c));
     return DMSGM_OK;
 }
 

@@ -48,7 +48,8 @@ class dmsgm_info(ctypes.Structure):
     _fields_ = [("width", ctypes.c_int), ("height", ctypes.c_int), ("block", ctypes.c_int),
                 ("blocks_x", ctypes.c_int), ("blocks_y", ctypes.c_int),
                 ("num_streams", ctypes.c_int), ("kernels_per_step", ctypes.c_int),
-                ("state_bytes", ctypes.c_size_t), ("algorithmic_bytes_per_frame", ctypes.c_double)]
+                ("state_bytes", ctypes.c_size_t), ("algorithmic_bytes_per_frame", ctypes.c_double),
+                ("kernel", ctypes.c_char * 64)]
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
