@@ -11,6 +11,8 @@ for r in rows[2:]:
     if len(r) < len(h) or not r[iS].split():
         continue
     t = r[iS].split(); op = t[1] if t[0].startswith("@") else t[0]
+    if not r[iT].isdigit():
+        continue
     ops[op] += int(r[iT]); tt += int(r[iT])
 print(f"thread instructions per unit: {tt / a.units:.1f}")
 for op, n in ops.most_common(a.top):
