@@ -50,10 +50,8 @@ def method_params(dm_or_oracle, S):
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", str(rank)))
-    return rank, world, local
+    from paper_1702_05156_b200.shard import env_rank
+    return env_rank()
 
 
 def measured_peak():
@@ -233,6 +231,7 @@ def run_dmsgm(args, rank, world, local):
 
     import paper_1702_05156_b200 as dm
     import synth
+    from paper_1702_05156_b200.shard import max_over_ranks, strong_shard, weak_shard
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -240,9 +239,12 @@ def run_dmsgm(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     wl = WORKLOADS[args.config]
     base = synth.config(wl["ring"])
-    S = base.S
-    # weak scaling: rank r owns streams [r*S, (r+1)*S) of the global batch
-    cfg = synth.config(wl["ring"], seed=base.seed + rank * S)
+    # weak scaling (default): rank r owns global streams [r*S, (r+1)*S); strong: the
+    # config's batch split across ranks.  Streams are independent: no data-path collective.
+    shard = (weak_shard(rank, world, base.S, local) if args.scaling == "weak"
+             else strong_shard(rank, world, base.S, local))
+    S = shard.num_streams
+    cfg = synth.config(wl["ring"], S=S, seed=base.seed + shard.first_stream)
     W, H, N = cfg.W, cfg.H, cfg.N
     frames, Hs = synth.generate_device(cfg, T=RING, device=f"cuda:{local}")    # [R][S][H][W] on device
     Hs_dev = torch.from_numpy(np.ascontiguousarray(Hs)).to(dev)
@@ -280,13 +282,10 @@ def run_dmsgm(args, rank, world, local):
     if world > 1:
         dist.barrier()
     ms_local = ev0.elapsed_time(ev1)
-    ms = ms_local
-    if world > 1:
-        t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms_local, dev)                     # the slowest rank sets the job time
     ms_per_step = ms / args.steps
-    frames_total = world * S * args.steps
+    total_streams = world * base.S if args.scaling == "weak" else base.S
+    frames_total = total_streams * args.steps
     fps = frames_total / (ms / 1e3)
     peak, peak_src = measured_peak()
     achieved = bytes_per_step / (ms_local / args.steps / 1e3) / 1e9     # GB/s, this rank's kernel
@@ -310,12 +309,8 @@ def run_dmsgm(args, rank, world, local):
             # the step's inputs are already in pinned host memory (written by the "producer"
             # outside the timed call); dmsgm_step_host copies H2D, computes, copies masks D2H
             ctx.step_host(ring_host[i % len(ring_host)], hH[i % RING], hm, stream)
-        e2e_s = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        e2e = {"value": world * S * e2e_steps / e2e_s, "unit": "frames/s",
+        e2e_s = max_over_ranks(time.perf_counter() - t0, dev)
+        e2e = {"value": total_streams * e2e_steps / e2e_s, "unit": "frames/s",
                "h2d_bytes_per_step": S * H * W + S * 9 * 8, "d2h_bytes_per_step": S * H * W,
                "steps": e2e_steps, "api": "dmsgm_step_host (pinned host buffers, synchronous)"}
 
@@ -341,10 +336,10 @@ def run_dmsgm(args, rank, world, local):
         line = {
             "metric": "frames/s", "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth/ ring recipe, generated on device)",
             "config": {"workload": args.config, "desc": wl["desc"], "W": W, "H": H, "N": N,
-                       "streams_per_gpu": S, "total_streams": world * S, "ring_frames": RING,
+                       "streams_per_gpu": S, "total_streams": total_streams, "ring_frames": RING,
                        "l2": f"inputs larger than L2: {bytes_per_step / 1e6:.1f} MB algorithmic traffic per step "
                              f"(ring of {RING} distinct frames/masks per stream, {2 * RING * S * W * H / 1e9:.2f} GB)",
                        "parallelism": f"stream-sharded x{world}, no data-path collective"},
@@ -376,6 +371,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU runs the config's batch (default); strong: the batch is split")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
