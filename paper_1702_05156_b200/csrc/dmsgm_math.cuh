@@ -103,6 +103,34 @@ DM_HD Interval bg_interval(float mu, float T, float r, bool may_be_empty = true)
     return iv;
 }
 
+// Fast form of bg_interval.  With r within 1.5e-4 of sqrt(T) (rsqrt estimate) and T <= 3e5,
+// |fl(mu +/- r) - (mu +/- sqrt(T))| < 2e-4, and the literal predicate can only differ from
+// exact arithmetic within ~5e-5 of k = mu +/- sqrt(T).  So when mu +/- r lies more than
+// 1e-3 away from an integer, floor(mu + r) / ceil(mu - r) ARE the interval ends; otherwise
+// (about 0.2% of blocks) the predicate-tested form decides.  Host-tested against the
+// literal predicate (tests/test_host_math.py).
+DM_HD bool interval_is_clear(float x) {
+    const float f = f_sub(x, floorf(x));
+    return f > 1e-3f && f < 0.999f;
+}
+
+DM_HD Interval bg_interval_fast(float mu, float T, float r, bool may_be_empty, bool* slow) {
+    const float hi_f = f_add(mu, r);
+    const float lo_f = f_sub(mu, r);
+    const bool clear = interval_is_clear(hi_f) && interval_is_clear(lo_f) && T <= 3.0e5f &&
+                       hi_f > -1.0f && lo_f < 256.0f;
+    *slow = !clear;
+    Interval iv;
+    int b = (int)floorf(hi_f);
+    int a = (int)ceilf(lo_f);
+    a = a < 0 ? 0 : a;
+    b = b > 255 ? 255 : b;
+    iv.a = a > b ? 256 : a;     // (may_be_empty only matters on the slow path: an empty
+    iv.b = b < 0 ? 0 : b;       //  interval has no integer in (lo_f, hi_f) -> a > b here)
+    (void)may_be_empty;
+    return iv;
+}
+
 // Per-16-bit-lane keys of an interval: x = lane + (0x8000 - a) has bit 15 set iff
 // lane >= a; y = (0x8000 + b) - lane has bit 15 set iff lane <= b (lanes <= 255, so no
 // carry/borrow crosses a lane).  a = 256 makes x's bit 15 always clear (all foreground).
