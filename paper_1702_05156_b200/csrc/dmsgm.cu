@@ -76,6 +76,20 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // 4-D view of a state buffer: {24 floats of a chunk, chunks per row, block rows, streams}.
+// 3-D view of a frame batch: {width bytes, rows, streams}; box 256 B x rows x 1.
+bool encode_frame_map(const dmsgm_ctx* c, const uint8_t* base, size_t pitch, int count, int box_rows,
+                      CUtensorMap* out) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)c->W, (cuuint64_t)c->H, (cuuint64_t)count};
+    cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * c->H};
+    cuuint32_t box[3] = {256, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_state_map(const dmsgm_ctx* c, float* base, int xc, int wrows, CUtensorMap* out) {
     auto enc = tensor_map_encoder();
     if (!enc) return false;
@@ -101,10 +115,11 @@ cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames
     sa.tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
     sa.items = count * sa.tiles_xc * sa.tiles_y;
     sa.s0 = s0;
-    (void)frames; (void)fpitch;
+    CUtensorMap fmap;
+    if (!encode_frame_map(c, frames, fpitch, count, N * kCtaY, &fmap)) return cudaErrorInvalidValue;
     const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
     dmsgm_step_staged<N, BPT, MINB, RULES><<<grid, dim3(kCtaX, kCtaY + 1, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(
-        a, sa, c->state_map[parity]);
+        a, sa, fmap, c->state_map[parity]);
     return cudaGetLastError();
 }
 
