@@ -15,8 +15,9 @@
  *   swap          Eq. 10 (App. E);
  *   mask          App. E P:655-663 with the variance reading R14.
  *
- * Arithmetic: fp32 state (north_star: "fp32 means/variances"), fp64 for the
- * projection only (R17); the decay exp is a fixed fp32 sequence (R18).  Built
+ * Arithmetic: fp32 throughout (north_star: "fp32 means/variances"); the
+ * projection is in displacement form (R17), the decay exp a fixed fp32
+ * sequence (R18); fp64 only converts the homography.  Built
  * with -O2 -ffp-contract=off -fno-fast-math: every + - * / below is one IEEE
  * round-to-nearest operation evaluated in the order written; fused
  * multiply-adds appear only where written as fma()/fmaf() (correctly rounded,
@@ -57,33 +58,40 @@ static float* stream_state(const dmsgm_oracle_ctx* c, int buf, int s) {
  * S1: project the block centre through H and find the up-to-4 source blocks
  * with their overlap (bilinear) weights.  Readings R2 (coordinates), R3 (H maps
  * frame t -> frame t-1), R4 (axis-aligned N x N footprint centred at H(c)),
- * R5 (out-of-range sources dropped; exposed block if w <= 0, far out, or no
- * in-range source has weight).  Returns 1 if exposed.
+ * R5 (out-of-range sources dropped; exposed block if w <= 0, if the displacement
+ * is not finite / beyond 2^20 blocks, or if no in-range source has weight), R17
+ * (displacement form in fp32: with g = H - I and e = w - 1,
+ *   (x' - X) w = g0 X + g1 Y + g2 - X e,   (y' - Y) w = g3 X + g4 Y + g5 - Y e,
+ * so the block-unit displacement (ex, ey) = ((x'-X)/N, (y'-Y)/N) keeps ~1e-7
+ * accuracy for the near-identity homographies of a moving camera).
+ * Returns 1 if exposed.
  * ---------------------------------------------------------------------- */
 static int project_block(int Wb, int Hb, int N, const double* h, int bi, int bj,
                          int kx[4], int ky[4], float Wt[4], float* sumW, int* clipped) {
-    double X = (double)N * (double)bi + (double)N / 2.0; /* block centre, R2 */
-    double Y = (double)N * (double)bj + (double)N / 2.0;
-    /* homogeneous image of the centre: (xn, yn, w) = H (X, Y, 1), each row as
-     * h_i0*X + (h_i1*Y + h_i2) with fused multiply-adds (R17) */
-    double w = fma(h[6], X, fma(h[7], Y, h[8]));
-    if (!(w > 0.0)) return 1;
-    double xn = fma(h[0], X, fma(h[1], Y, h[2]));
-    double yn = fma(h[3], X, fma(h[4], Y, h[5]));
-    double rw = 1.0 / w;
-    double xp = xn * rw; /* frame t-1 pixel coordinates of the centre */
-    double yp = yn * rw;
-    double u = xp / (double)N; /* source block-grid coordinates: block k covers [k, k+1) */
-    double v = yp / (double)N;
-    if (!(u > -2.0 && u < (double)Wb + 2.0 && v > -2.0 && v < (double)Hb + 2.0)) return 1;
-    double ku = floor(u);
-    double kv = floor(v);
-    double du = u - (ku + 0.5); /* offset of the footprint centre from the source block centre */
-    double dv = v - (kv + 0.5);
-    int su = du > 0.0 ? 1 : -1;
-    int sv = dv > 0.0 ? 1 : -1;
-    float a = (float)fabs(du);
-    float b = (float)fabs(dv);
+    const float g0 = (float)(h[0] - 1.0), g1 = (float)h[1], g2 = (float)h[2];
+    const float g3 = (float)h[3], g4 = (float)(h[4] - 1.0), g5 = (float)h[5];
+    const float g6 = (float)h[6], g7 = (float)h[7], g8 = (float)(h[8] - 1.0);
+    float X = (float)(N * bi) + (float)N / 2.0f; /* block centre, R2 (exact in fp32) */
+    float Y = (float)(N * bj) + (float)N / 2.0f;
+    float e = fmaf(g6, X, fmaf(g7, Y, g8));      /* w - 1 */
+    float w = 1.0f + e;
+    if (!(w > 0.0f)) return 1;
+    float px = fmaf(-X, e, fmaf(g0, X, fmaf(g1, Y, g2)));
+    float py = fmaf(-Y, e, fmaf(g3, X, fmaf(g4, Y, g5)));
+    float rw = 1.0f / w;
+    float ex = (px * rw) / (float)N;             /* displacement of the centre in blocks */
+    float ey = (py * rw) / (float)N;
+    if (!(fabsf(ex) < 1048576.0f && fabsf(ey) < 1048576.0f)) return 1;
+    /* source block-grid coordinate u = bi + 1/2 + ex: block k covers [k, k+1) */
+    float tx = 0.5f + ex, ty = 0.5f + ey;
+    float fx = floorf(tx), fy = floorf(ty);
+    float du = (tx - fx) - 0.5f;                 /* offset of the footprint centre from the source block centre */
+    float dv = (ty - fy) - 0.5f;
+    int ku = bi + (int)fx, kv = bj + (int)fy;
+    int su = du > 0.0f ? 1 : -1;
+    int sv = dv > 0.0f ? 1 : -1;
+    float a = fabsf(du);
+    float b = fabsf(dv);
     float one_a = 1.0f - a;
     float one_b = 1.0f - b;
     /* overlap areas of the unit footprint with the 4 cells, order self, H, V, HV */
@@ -91,10 +99,10 @@ static int project_block(int Wb, int Hb, int N, const double* h, int bi, int bj,
     Wt[1] = a * one_b;
     Wt[2] = one_a * b;
     Wt[3] = a * b;
-    kx[0] = (int)ku;       ky[0] = (int)kv;
-    kx[1] = (int)ku + su;  ky[1] = (int)kv;
-    kx[2] = (int)ku;       ky[2] = (int)kv + sv;
-    kx[3] = (int)ku + su;  ky[3] = (int)kv + sv;
+    kx[0] = ku;       ky[0] = kv;
+    kx[1] = ku + su;  ky[1] = kv;
+    kx[2] = ku;       ky[2] = kv + sv;
+    kx[3] = ku + su;  ky[3] = kv + sv;
     *clipped = 0;
     for (int k = 0; k < 4; ++k)
         if (kx[k] < 0 || kx[k] >= Wb || ky[k] < 0 || ky[k] >= Hb) {
