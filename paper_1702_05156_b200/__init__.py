@@ -1,11 +1,20 @@
 """B200-native (sm_100a) grid-block Dual-Mode SGM motion masking (arXiv 1702.05156).
 
-The hot path lives in libdmsgm.so behind the C ABI of include/dmsgm.h; this
-package is the thin Python binding.  See DESIGN.md.
-"""
-from .dmsgm import (DMSGM_ECUDA, DMSGM_EINVAL, DMSGM_ENOMEM, DMSGM_ESTATE, DMSGM_OK, EXPORTS,
-                    Dmsgm, DmsgmError, Params, dmsgm_info, dmsgm_params, lib, load_library, version)
+The hot path lives in libdmsgm.so behind the C ABI of include/dmsgm.h; the binding is
+paper_1702_05156_b200.dmsgm.  See DESIGN.md.
 
-__all__ = ["Dmsgm", "DmsgmError", "Params", "dmsgm_params", "dmsgm_info", "lib", "load_library",
-           "version", "EXPORTS", "DMSGM_OK", "DMSGM_EINVAL", "DMSGM_ENOMEM", "DMSGM_ECUDA",
-           "DMSGM_ESTATE"]
+The binding is imported lazily so that `python -m paper_1702_05156_b200.build` works on
+a fresh checkout; touching any API name loads libdmsgm.so and raises ImportError when it
+is missing (there is no CPU fallback).
+"""
+_API = ("Dmsgm", "DmsgmError", "Params", "dmsgm_params", "dmsgm_info", "lib", "load_library", "version",
+        "EXPORTS", "DMSGM_OK", "DMSGM_EINVAL", "DMSGM_ENOMEM", "DMSGM_ECUDA", "DMSGM_ESTATE")
+
+__all__ = list(_API)
+
+
+def __getattr__(name):
+    if name in _API:
+        from . import dmsgm
+        return getattr(dmsgm, name)
+    raise AttributeError(name)

@@ -14,7 +14,8 @@ from dataclasses import dataclass, fields
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdmsgm.so")
+# DMSGM_LIB_PATH: load another build of the same C ABI (A/B timing of kernel versions)
+LIB_PATH = os.environ.get("DMSGM_LIB_PATH") or os.path.join(_PKG, "libdmsgm.so")
 
 DMSGM_OK = 0
 DMSGM_EINVAL = -1

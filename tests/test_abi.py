@@ -75,3 +75,15 @@ def test_binding_has_no_fallback():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(import\s+oracle|from\s+oracle|dmsgm_oracle|oracle/)", txt), f
+
+
+def test_build_from_clean_checkout(tmp_path):
+    """`python -m paper_1702_05156_b200.build` works without a prebuilt library."""
+    import shutil
+    import subprocess
+    import sys
+    shutil.copytree(os.path.join(ROOT, "include"), tmp_path / "include")
+    shutil.copytree(os.path.join(ROOT, "paper_1702_05156_b200"), tmp_path / "paper_1702_05156_b200",
+                    ignore=shutil.ignore_patterns("*.so", "__pycache__"))
+    subprocess.check_call([sys.executable, "-m", "paper_1702_05156_b200.build"], cwd=tmp_path, timeout=600)
+    assert (tmp_path / "paper_1702_05156_b200" / "libdmsgm.so").exists()
