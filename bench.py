@@ -239,6 +239,8 @@ def run_dmsgm(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     wl = WORKLOADS[args.config]
     base = synth.config(wl["ring"])
+    if args.streams:
+        base = synth.config(wl["ring"], S=args.streams)
     # weak scaling (default): rank r owns global streams [r*S, (r+1)*S); strong: the
     # config's batch split across ranks.  Streams are independent: no data-path collective.
     shard = (weak_shard(rank, world, base.S, local) if args.scaling == "weak"
@@ -371,6 +373,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="override streams per GPU (profiling only; the bench workload is the config's)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every GPU runs the config's batch (default); strong: the batch is split")
     args = ap.parse_args()

@@ -58,6 +58,7 @@ struct dmsgm_ctx {
     int staged;        // 1: persistent TMA-staged kernel (N = 4, N = 8)
     int staged_ctas;   // resident CTAs of the staged kernel on this device
     int staged_occ;    // register-capped occupancy variant (3 or 4 CTAs/SM)
+    int staged_ftma;   // 1: frames staged by TMA (2-stage ring); 0: 3-stage window ring + register prefetch
     CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (chunk-SoA, 4-D)
     char err[512];
 };
@@ -107,7 +108,7 @@ bool encode_state_map(const dmsgm_ctx* c, float* base, int xc, int wrows, CUtens
 }  // namespace
 
 // Persistent TMA-staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
-template <int N, int BPT, int MINB, bool RULES>
+template <int N, int BPT, int MINB, bool RULES, bool FTMA>
 cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames, size_t fpitch, int s0,
                           int count, int parity, cudaStream_t stream) {
     StagedArgs sa;
@@ -118,28 +119,29 @@ cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames
     CUtensorMap fmap;
     if (!encode_frame_map(c, frames, fpitch, count, N * kCtaY, &fmap)) return cudaErrorInvalidValue;
     const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
-    dmsgm_step_staged<N, BPT, MINB, RULES><<<grid, dim3(kCtaX, kCtaY + 1, 1), Staged<N, BPT>::SMEM_BYTES, stream>>>(
+    dmsgm_step_staged<N, BPT, MINB, RULES, FTMA><<<grid, dim3(kCtaX, kCtaY + 1, 1), Staged<N, BPT, FTMA>::SMEM_BYTES,
+                                                   stream>>>(
         a, sa, fmap, c->state_map[parity]);
     return cudaGetLastError();
 }
 
-template <int N, int BPT, int MINB>
+template <int N, int BPT, int MINB, bool FTMA>
 cudaError_t setup_staged(dmsgm_ctx* c) {
-    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT>::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, FTMA>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Staged<N, BPT>::SMEM_BYTES);
+        e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, FTMA>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB, false>,
-                                                      kStagedThreads, Staged<N, BPT>::SMEM_BYTES);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB, false, FTMA>,
+                                                      kStagedThreads, Staged<N, BPT, FTMA>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     if (e != cudaSuccess) return e;
     c->staged_ctas = (per_sm > 0 ? per_sm : 1) * sms;
     for (int i = 0; i < 2; ++i)
-        if (!encode_state_map(c, c->state[i], Staged<N, BPT>::XC, Staged<N, BPT>::WROWS, &c->state_map[i]))
+        if (!encode_state_map(c, c->state[i], Staged<N, BPT, FTMA>::XC, Staged<N, BPT, FTMA>::WROWS, &c->state_map[i]))
             return cudaErrorInvalidValue;
     return cudaSuccess;
 }
@@ -270,18 +272,21 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
         // RULES = the App. E compatibility switches (R27/R28) are on: runtime-switched code;
         // otherwise the default rules are compiled in without branches.
         const bool rules = c->p.update_rule != 0 || c->p.classify_rule != 0;
-        const bool o3 = c->staged_occ == 3;
-#define DMSGM_STAGED(NN, BB, OO)                                                                   \
-    return rules ? launch_staged<NN, BB, OO, true>(c, a, frames, fpitch, s0, count, parity, stream) \
-                 : launch_staged<NN, BB, OO, false>(c, a, frames, fpitch, s0, count, parity, stream)
+#define DMSGM_STAGED(NN, BB, OO, FT)                                                                        \
+    return rules ? launch_staged<NN, BB, OO, true, FT>(c, a, frames, fpitch, s0, count, parity, stream)    \
+                 : launch_staged<NN, BB, OO, false, FT>(c, a, frames, fpitch, s0, count, parity, stream)
+#define DMSGM_STAGED_OCC(NN, BB, FT)       \
+    if (c->staged_occ == 3) DMSGM_STAGED(NN, BB, 3, FT); \
+    DMSGM_STAGED(NN, BB, 4, FT)
         if (c->N == 4) {
-            if (o3) DMSGM_STAGED(4, 2, 3);
-            DMSGM_STAGED(4, 2, 4);
+            if (c->staged_ftma) { DMSGM_STAGED_OCC(4, 2, true); }
+            DMSGM_STAGED_OCC(4, 2, false);
         }
         if (c->N == 8) {
-            if (o3) DMSGM_STAGED(8, 1, 3);
-            DMSGM_STAGED(8, 1, 4);
+            if (c->staged_ftma) { DMSGM_STAGED_OCC(8, 1, true); }
+            DMSGM_STAGED_OCC(8, 1, false);
         }
+#undef DMSGM_STAGED_OCC
 #undef DMSGM_STAGED
     }
     switch (c->N * 16 + bpt) {
@@ -362,8 +367,13 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
         if (want && (block == 4 || block == 8)) {
             const char* oenv = getenv("DMSGM_STAGED_OCC");   // 3 or 4 resident CTAs per SM (register cap)
             c->staged_occ = (oenv && atoi(oenv) == 4) ? 4 : 3;
-            if (c->staged_occ == 3) e = block == 4 ? setup_staged<4, 2, 3>(c) : setup_staged<8, 1, 3>(c);
-            else e = block == 4 ? setup_staged<4, 2, 4>(c) : setup_staged<8, 1, 4>(c);
+            const char* fenv = getenv("DMSGM_STAGED_FRAMES");  // "tma" (default) or "regs"
+            c->staged_ftma = !(fenv && strcmp(fenv, "regs") == 0);
+#define DMSGM_SETUP(NN, BB)                                                                   \
+    (c->staged_ftma ? (c->staged_occ == 3 ? setup_staged<NN, BB, 3, true>(c) : setup_staged<NN, BB, 4, true>(c)) \
+                    : (c->staged_occ == 3 ? setup_staged<NN, BB, 3, false>(c) : setup_staged<NN, BB, 4, false>(c)))
+            e = block == 4 ? DMSGM_SETUP(4, 2) : DMSGM_SETUP(8, 1);
+#undef DMSGM_SETUP
             if (e != cudaSuccess) {
                 dmsgm_destroy(c);
                 return fail(nullptr, DMSGM_ECUDA, "staged kernel setup: %s", cudaGetErrorString(e));
@@ -574,8 +584,8 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     // frame read (1 B/px) + mask write (1 B/px) + state read + write (2 x 24 B per block)
     out->algorithmic_bytes_per_frame = 2.0 * c->W * c->H + 2.0 * 24.0 * (double)plane_elems(c);
     if (c->staged)
-        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d> (TMA, persistent)", c->N,
-                 c->N == 4 ? 2 : 1, c->staged_occ);
+        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d,%s> (TMA, persistent)", c->N,
+                 c->N == 4 ? 2 : 1, c->staged_occ, c->staged_ftma ? "frames:tma" : "frames:regs");
     else
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_kernel<%d,%d>", c->N, bpt_of(c));
     return DMSGM_OK;
