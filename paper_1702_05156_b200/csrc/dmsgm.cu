@@ -59,6 +59,7 @@ struct dmsgm_ctx {
     int staged_ctas;   // resident CTAs of the staged kernel on this device
     int staged_occ;    // register-capped occupancy variant (3 or 4 CTAs/SM)
     int staged_ftma;   // 1: frames staged by TMA (2-stage ring); 0: 3-stage window ring + register prefetch
+    int pdl;           // programmatic dependent launch of consecutive steps (DMSGM_PDL=0 disables)
     CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (chunk-SoA, 4-D)
     char err[512];
 };
@@ -119,10 +120,19 @@ cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames
     CUtensorMap fmap;
     if (!encode_frame_map(c, frames, fpitch, count, N * kCtaY, &fmap)) return cudaErrorInvalidValue;
     const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
-    dmsgm_step_staged<N, BPT, MINB, RULES, FTMA><<<grid, dim3(kCtaX, kCtaY + 1, 1), Staged<N, BPT, FTMA>::SMEM_BYTES,
-                                                   stream>>>(
-        a, sa, fmap, c->state_map[parity]);
-    return cudaGetLastError();
+    // programmatic dependent launch: may begin while the previous step drains; the kernel
+    // itself waits (griddepcontrol.wait) before touching the state the previous step wrote
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kCtaX, kCtaY + 1, 1);
+    cfg.dynamicSmemBytes = Staged<N, BPT, FTMA>::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, dmsgm_step_staged<N, BPT, MINB, RULES, FTMA>, a, sa, fmap, c->state_map[parity]);
 }
 
 template <int N, int BPT, int MINB, bool FTMA>
@@ -367,6 +377,8 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
         if (want && (block == 4 || block == 8)) {
             const char* oenv = getenv("DMSGM_STAGED_OCC");   // 3 or 4 resident CTAs per SM (register cap)
             c->staged_occ = (oenv && atoi(oenv) == 4) ? 4 : 3;
+            const char* penv = getenv("DMSGM_PDL");
+            c->pdl = !(penv && atoi(penv) == 0);
             const char* fenv = getenv("DMSGM_STAGED_FRAMES");  // "tma" (default) or "regs"
             c->staged_ftma = !(fenv && strcmp(fenv, "regs") == 0);
 #define DMSGM_SETUP(NN, BB)                                                                   \
