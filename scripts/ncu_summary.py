@@ -49,6 +49,9 @@ def main():
     ap.add_argument("tag")
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--bench", default=None)
+    ap.add_argument("--scale", type=float, default=1.0,
+                    help="multiply DRAM bytes (capture taken on a smaller batch of the same workload)")
+    ap.add_argument("--note", default="")
     args = ap.parse_args()
     go = os.path.join(ROOT, "gpurun_out")
     prof = os.path.join(go, f"prof_{args.tag}.ncu-rep")
@@ -66,7 +69,7 @@ def main():
             if m in hdr:
                 rec[m] = (d[hdr.index(m)], units[hdr.index(m)])
         per_launch.append(rec)
-    lines.append(f"Source: `ncu --set full --clock-control none --import-source on -k regex:dmsgm_step_kernel` "
+    lines.append(f"Source: `ncu --set full --clock-control none --import-source on -k regex:dmsgm_step` "
                  f"({len(per_launch)} launches captured; one row per launch).")
     lines.append("")
     lines.append("| metric | unit | " + " | ".join(f"launch {i}" for i in range(len(per_launch))) + " |")
@@ -83,8 +86,9 @@ def main():
         return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1.0) if scale else f
 
     dram = [num(r, "dram__bytes_read.sum", True) + num(r, "dram__bytes_write.sum", True) for r in per_launch]
-    dram_per_launch = sum(dram) / len(dram)
-    lines.append(f"DRAM bytes per launch (read + write, mean): **{dram_per_launch / 1e6:.1f} MB**")
+    dram_per_launch = sum(dram) / len(dram) * args.scale
+    lines.append(f"DRAM bytes per launch (read + write, mean{', x%g' % args.scale if args.scale != 1 else ''}): "
+                 f"**{dram_per_launch / 1e6:.1f} MB** {args.note}")
 
     # SASS opcode histogram of the first captured launch (dynamic warp instructions)
     srows = ncu_csv(["-i", prof, "--page", "source", "--csv", "--print-source", "sass"])
@@ -140,7 +144,7 @@ def main():
         f.write("\n".join(lines) + "\n")
     with open(os.path.join(prof_dir, f"ncu_traffic_{args.workload}.json"), "w") as f:
         json.dump({"dram_bytes_per_launch": dram_per_launch, "source": f"profiles/{args.tag}_ncu_summary.md",
-                   "tag": args.tag}, f, indent=1)
+                   "tag": args.tag, "scale": args.scale, "note": args.note}, f, indent=1)
     print("\n".join(lines))
 
 
