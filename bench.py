@@ -1,7 +1,9 @@
 """DMSGM step benchmark (BASELINE.json metric: frames/s and Mpixel/s per DMSGM step, % of HBM roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4|C5] [--impl dmsgm|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4|C5|C5b] [--impl dmsgm|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+    python bench.py --config C5b --bands 8                  (8 row bands of one 4K frame on 1 GPU)
+    torchrun --nproc-per-node 8 bench.py --config C5b [--exchange peer|nccl]
 
 A "step" is one pass of the whole hot path (warp/mix + block mean + dual-mode update +
 mask, one fused kernel launch) over one batch of S streams x 1 frame.  Workload C4:
@@ -38,6 +40,7 @@ FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (use
 WORKLOADS = {
     "C4": dict(ring="C4ring", desc="1920x1080 u8, 4x4 blocks, 32 streams/GPU"),
     "C5": dict(ring="C5ring", desc="3840x2160 u8, 8x8 blocks, 64 streams/GPU"),
+    "C5b": dict(ring="C5bring", desc="3840x2160 u8, 8x8 blocks, ONE stream split into row bands"),
 }
 
 
@@ -362,6 +365,179 @@ def run_dmsgm(args, rank, world, local):
     return 0
 
 
+# ---------------------------------------------------------------------------
+def run_band(args, rank, world, local):
+    """C5b: one 4K stream per step, its block rows split into bands.
+    Under torchrun: band = rank, one GPU each, neighbours exchanged by the fused peer
+    stores + sync kernel (--exchange peer, CUDA IPC) or by NCCL send/recv (--exchange
+    nccl, the baseline).  On one process: --bands G bands on this GPU, one CUDA stream
+    each (peer pointers, same protocol).  Strong scaling: the frame is fixed."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1702_05156_b200 as dm
+    import synth
+    from paper_1702_05156_b200.band import BandGroup, BandRank, band_rows, halo_for
+    from paper_1702_05156_b200.shard import max_over_ranks
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = WORKLOADS[args.config]
+    cfg = synth.config(wl["ring"])
+    W, H, N = cfg.W, cfg.H, cfg.N
+    if world > 1 and args.bands not in (0, world):
+        raise SystemExit("--bands must equal the number of ranks under torchrun")
+    G = world if world > 1 else max(1, args.bands)
+    bands = band_rows(H // N, G)
+    frames, Hs = synth.generate_device(cfg, T=RING, device=f"cuda:{local}")    # [R][1][H][W]
+    Hs_dev = torch.from_numpy(np.ascontiguousarray(Hs)).to(dev)
+    halo = halo_for(W, H, N, Hs.reshape(-1, 9), bands)
+    masks = torch.empty_like(frames)
+    params = method_params(dm, 1)
+    main_stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        br = BandRank(W, H, N, params, rank, world, halo, device=local, exchange=args.exchange)
+        ctxs, my_bands = [br.ctx], [br.band]
+        sl = slice(br.band.row0 * N, br.band.row1 * N)
+        streams = [main_stream]
+
+        def step(i):
+            r = i % RING
+            br.step(frames[r][:, sl], Hs_dev[r], masks[r][:, sl])
+    else:
+        streams = [torch.cuda.Stream(dev) for _ in range(G)] if G > 1 else [main_stream]
+        grp = BandGroup(W, H, N, params, G, halo, device=local, streams=streams if G > 1 else None)
+        ctxs, my_bands = grp.ctxs, grp.bands
+
+        def step(i):
+            r = i % RING
+            grp.step(frames[r], Hs_dev[r], masks[r])
+    bytes_per_step = sum(c.info.algorithmic_bytes_per_frame for c in ctxs)
+    launches_per_step = sum(c.info.kernels_per_step for c in ctxs)
+    kernel_name = ctxs[0].info.kernel.decode()
+
+    def fork():
+        for st in streams:
+            if st is not main_stream:
+                st.wait_stream(main_stream)
+
+    def join():
+        for st in streams:
+            if st is not main_stream:
+                main_stream.wait_stream(st)
+
+    fork()
+    for i in range(args.warmup):
+        step(i)
+    join()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        torch.cuda.nvtx.range_push("timed")
+        ev0.record(main_stream)
+        fork()
+        for i in range(args.steps):
+            step(args.warmup + i)
+        join()
+        ev1.record(main_stream)
+        torch.cuda.nvtx.range_pop()
+        sampler.sample_once()
+        ev1.synchronize()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms_local, dev)
+    fps = args.steps / (ms / 1e3)
+    peak, peak_src = measured_peak()
+    achieved = bytes_per_step / (ms_local / args.steps / 1e3) / 1e9
+    status = [c.get_status() for c in ctxs]
+
+    # ---- end to end: pinned host frame -> device, band steps, masks -> pinned host ----
+    e2e = None
+    if not args.no_e2e:
+        y0, y1 = my_bands[0].row0 * N, my_bands[-1].row1 * N
+        hf = [frames[r][:, y0:y1].cpu().pin_memory() for r in range(2)]
+        hm = torch.empty((1, y1 - y0, W), dtype=torch.uint8, pin_memory=True)
+        e2e_steps = max(3, min(args.steps, args.e2e_steps))
+
+        def e2e_step(i):
+            r = i % 2
+            frames[r][:, y0:y1].copy_(hf[r], non_blocking=True)
+            fork()
+            step(r)
+            join()
+            hm.copy_(masks[r][:, y0:y1], non_blocking=True)
+            torch.cuda.synchronize(dev)
+        for i in range(3):
+            e2e_step(i)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(e2e_steps):
+            e2e_step(i)
+        e2e_s = max_over_ranks(time.perf_counter() - t0, dev)
+        e2e = {"value": e2e_steps / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": (y1 - y0) * W,
+               "d2h_bytes_per_step": (y1 - y0) * W, "steps": e2e_steps,
+               "api": "band step (BandGroup/BandRank.step) between pinned-host copies, synchronous"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        fh = frames[:2].cpu().numpy()
+        per_frame = 0.021 * (W * H) / (1920 * 1080)
+        nf = max(2, int(args.cpu_seconds / per_frame))
+        cfps, used, wall = oracle_throughput(cfg, fh, Hs[:2], 1, nf, 1)
+        cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle",
+               "sample": f"1 stream x {nf} frames of 3840x2160 (N={N}), whole frame, {wall:.1f} s wall, "
+                         f"single-threaded oracle"}
+    clocks = sampler.summary()
+    for c in ctxs:
+        c.close()
+    if rank == 0:
+        if G == 1:
+            exch = "none (one band)"
+        elif world == 1:
+            exch = "fused peer stores + sync kernel (one GPU, one CUDA stream per band)"
+        elif args.exchange == "peer":
+            exch = "fused peer stores + sync kernel (CUDA IPC over NVLink)"
+        else:
+            exch = "NCCL send/recv of the halo rows (baseline)"
+        line = {
+            "metric": "frames/s", "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (synth/ C5bring recipe, generated on device)",
+            "config": {"workload": args.config, "desc": wl["desc"], "W": W, "H": H, "N": N, "bands": G,
+                       "band_rows": [b.rows for b in bands], "halo_rows": halo, "exchange": exch,
+                       "ring_frames": RING,
+                       "l2": f"ring of {RING} distinct 4K frames + masks ({2 * RING * W * H / 1e6:.0f} MB) > L2; "
+                             f"the 2 x 3.1 MB state of a band context is L2-resident",
+                       "parallelism": f"row bands x{G} of one stream"},
+            "mpixel_per_s": fps * W * H / 1e6,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": bytes_per_step, "peak_source": peak_src,
+                         "kernel": f"{kernel_name} x{len(ctxs)} + band sync",
+                         "note": "one 4K frame is 2.9-23 MB of traffic per GPU per step: latency-bound"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "band_status": status,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -377,12 +553,18 @@ def main():
                     help="override streams per GPU (profiling only; the bench workload is the config's)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every GPU runs the config's batch (default); strong: the batch is split")
+    ap.add_argument("--bands", type=int, default=0,
+                    help="C5b: row bands (default: one per rank; on one process, G bands on this GPU)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="C5b under torchrun: fused peer stores + sync kernel, or NCCL send/recv baseline")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.config == "C5b":
+        return run_band(args, rank, world, local)
     return run_dmsgm(args, rank, world, local)
 
 

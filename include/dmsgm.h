@@ -46,7 +46,8 @@ extern "C" {
                             invalid state values in dmsgm_set_state                      */
 #define DMSGM_ENOMEM  -2 /* device or host allocation failed                             */
 #define DMSGM_ECUDA   -3 /* CUDA runtime error (no device, launch failure, async fault)   */
-#define DMSGM_ESTATE  -4 /* stream index out of range                                    */
+#define DMSGM_ESTATE  -4 /* stream index out of range; row band: halo too small, band/peer
+                            configuration invalid                                         */
 
 /* Parameters of the method (all explicit; there are no hidden defaults in the kernel). */
 typedef struct {
@@ -70,9 +71,11 @@ typedef struct {
     int width, height, block;      /* W, H, N                                   */
     int blocks_x, blocks_y;        /* Wb = W/N, Hb = H/N                        */
     int num_streams;               /* S                                         */
-    int kernels_per_step;          /* kernel launches per dmsgm_step (1)       */
+    int kernels_per_step;          /* kernel launches per step: 1 (+1 band sync with neighbours) */
+    int band_row0, band_rows, band_halo; /* row band (0, Hb, 0 for the whole frame)    */
     size_t state_bytes;            /* one state buffer (internal chunk-SoA layout, padded to Wb%4) */
-    double algorithmic_bytes_per_frame; /* frame read + mask write + state read+write, one stream */
+    double algorithmic_bytes_per_frame; /* frame read + mask write + state read+write, one stream
+                                           (band: its rows + the halo rows sent to neighbours) */
     char kernel[64];               /* the kernel dmsgm_step launches, e.g. "dmsgm_step_staged<4,2>" */
 } dmsgm_info;
 
@@ -133,6 +136,77 @@ const char* dmsgm_last_error(const dmsgm_ctx* ctx);
 
 /* Free all device/host resources of the context (synchronises the device). */
 void dmsgm_destroy(dmsgm_ctx* ctx);
+
+/* ------------------------------------------------------------------------------------
+ * Row-band split of one large frame over several GPUs (
+ * north_star: "a single very large frame may optionally be split into row bands with
+ * a one-block-row halo exchanged over NVLink").  Only S1-S2 read neighbouring blocks
+ * (the warp/mix of the previous models, §2.4), so a band needs the previous
+ * state of `halo` block rows above and below it; S4-S8 touch only its own pixels.
+ *
+ * Every band context keeps the full-grid state layout (rows outside band + halo are
+ * never read).  Its step kernel writes its first / last `halo` rows of the new state
+ * into the upper / lower neighbour's next-state buffer as well (direct stores, peer
+ * memory over NVLink / NVSwitch when the neighbour is on another GPU), and
+ * dmsgm_band_sync then publishes "step done" to the neighbours and waits for theirs.
+ * Results are bitwise equal to the whole-frame step.
+ * ------------------------------------------------------------------------------------ */
+
+/* Make `ctx` process block rows [row0, row0 + rows) only (0 <= row0, rows >= 1,
+ * row0 + rows <= Hb; 0 <= halo <= rows).  Afterwards frames and masks passed to the step
+ * calls hold the band's pixel rows only: u8 [S][rows*N][pitch], pixel row 0 = global
+ * pixel row row0*N; homographies stay in whole-frame coordinates.  Detaches any
+ * neighbour, zeroes the sync counters and status, marks every stream fresh.  (0, Hb, 0)
+ * restores whole-frame mode.  All bands of one frame must use the same halo.
+ * Synchronises the device. */
+int dmsgm_set_band(dmsgm_ctx* ctx, int row0, int rows, int halo);
+
+/* Device buffers a neighbour needs (same process). */
+typedef struct {
+    void* state[2];      /* the two state ping-pong buffers (internal layout)            */
+    void* flags;         /* 3 x u32 sync words                                            */
+    int parity;          /* index of the buffer holding the current state                */
+    unsigned steps;      /* steps completed by this context                               */
+    size_t row_bytes;    /* bytes of one block row of one stream in a state buffer        */
+    size_t stream_bytes; /* bytes of one stream in a state buffer                         */
+} dmsgm_buffers;
+int dmsgm_get_buffers(const dmsgm_ctx* ctx, dmsgm_buffers* out);
+
+/* Attach the neighbour band on `side` (0: the band above, ending at row0; 1: the band
+ * below, starting at row0 + rows) from its dmsgm_get_buffers (pointers valid on this
+ * context's device: same device, or peer access enabled); NULL detaches.  Both bands
+ * must have the same width, block, num_streams and halo, and must be stepped in
+ * lockstep (same number of steps) from their set_band on. */
+int dmsgm_attach_peer(dmsgm_ctx* ctx, int side, const dmsgm_buffers* peer);
+
+/* Cross-process form: DMSGM_IPC_BYTES bytes of CUDA IPC handles for the two state
+ * buffers and the sync words (written to `out`), and the attach that opens them. */
+#define DMSGM_IPC_BYTES 192
+int dmsgm_get_ipc_handles(const dmsgm_ctx* ctx, void* out, size_t out_bytes);
+int dmsgm_attach_peer_ipc(dmsgm_ctx* ctx, int side, const void* handles, size_t bytes);
+
+/* After a step: publish this context's step count to its neighbours (signal), wait
+ * until every attached neighbour has completed the same step (wait), or both in one
+ * launch (sync).  One single-thread kernel on `cuda_stream`; asynchronous.  A wait
+ * longer than DMSGM_BAND_TIMEOUT_MS (env, default 10000) gives up and records a
+ * timeout in the status word.  dmsgm_step_n issues the sync after every step itself
+ * when neighbours are attached.  With several bands on ONE stream, enqueue all steps,
+ * then all signals, then all waits (a wait blocks the stream behind it). */
+int dmsgm_band_signal(dmsgm_ctx* ctx, void* cuda_stream);
+int dmsgm_band_wait(dmsgm_ctx* ctx, void* cuda_stream);
+int dmsgm_band_sync(dmsgm_ctx* ctx, void* cuda_stream);
+
+/* Status word (synchronises the device), then clears it: bit 0 = a positive-weight
+ * source lay outside the band + halo (the masks / state of that step are not valid),
+ * bit 1 = a neighbour wait timed out.  Any set bit also makes the next step call fail
+ * (DMSGM_ESTATE / DMSGM_ECUDA) until it is read here or the band is set again. */
+int dmsgm_get_status(dmsgm_ctx* ctx, unsigned* out);
+
+/* Host helper: the halo (block rows) that band [row0, row0 + rows) needs for the given
+ * HOST homographies f64 [count][9]: max distance of a positive-weight source row from
+ * the band, by the same fp32 projection as the kernel (S1, R17). */
+int dmsgm_band_halo_needed(int width, int height, int block, const double* host_homographies, int count,
+                           int row0, int rows, int* out);
 
 /* Library version string, e.g. "dmsgm-b200 0.1 sm_100a". */
 const char* dmsgm_version(void);

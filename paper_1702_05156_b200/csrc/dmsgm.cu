@@ -61,6 +61,16 @@ struct dmsgm_ctx {
     int staged_ftma;   // 1: frames staged by TMA (2-stage ring); 0: 3-stage window ring + register prefetch
     int pdl;           // programmatic dependent launch of consecutive steps (DMSGM_PDL=0 disables)
     CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (chunk-SoA, 4-D)
+    // row band; whole frame: row0 = 0, rows = Hb, halo = 0, band = 0
+    int band, row0, rows, halo;
+    int Hp;                      // pixel rows of the frames / masks passed to a step (rows * N)
+    unsigned steps;              // completed steps (host count; the device epoch is flags[2])
+    unsigned* flags;             // device [3]: from upper, from lower, own epoch (band sync)
+    unsigned* status_host;       // host-mapped status word: bit 0 halo overflow, bit 1 peer timeout
+    unsigned* status_dev;
+    float* peer_state[2][2];     // [side][buffer]: neighbours' state buffers (side 0 upper, 1 lower)
+    unsigned* peer_slot[2];      // neighbour's flag word that we signal
+    void* ipc_open[2][3];        // IPC mappings to close at destroy
     char err[512];
 };
 
@@ -83,8 +93,8 @@ bool encode_frame_map(const dmsgm_ctx* c, const uint8_t* base, size_t pitch, int
                       CUtensorMap* out) {
     auto enc = tensor_map_encoder();
     if (!enc) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)c->W, (cuuint64_t)c->H, (cuuint64_t)count};
-    cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * c->H};
+    cuuint64_t dims[3] = {(cuuint64_t)c->W, (cuuint64_t)c->Hp, (cuuint64_t)count};
+    cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * c->Hp};
     cuuint32_t box[3] = {256, (cuuint32_t)box_rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, es,
@@ -109,12 +119,12 @@ bool encode_state_map(const dmsgm_ctx* c, float* base, int xc, int wrows, CUtens
 }  // namespace
 
 // Persistent TMA-staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
-template <int N, int BPT, int MINB, bool RULES, bool FTMA>
+template <int N, int BPT, int MINB, bool RULES, bool FTMA, bool BAND = false>
 cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames, size_t fpitch, int s0,
                           int count, int parity, cudaStream_t stream) {
     StagedArgs sa;
     sa.tiles_xc = (c->Wb + Staged<N, BPT>::TWB - 1) / Staged<N, BPT>::TWB;
-    sa.tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
+    sa.tiles_y = (c->rows + kCtaY - 1) / kCtaY;
     sa.items = count * sa.tiles_xc * sa.tiles_y;
     sa.s0 = s0;
     CUtensorMap fmap;
@@ -132,19 +142,28 @@ cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames
     attr[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, dmsgm_step_staged<N, BPT, MINB, RULES, FTMA>, a, sa, fmap, c->state_map[parity]);
+    return cudaLaunchKernelEx(&cfg, dmsgm_step_staged<N, BPT, MINB, RULES, FTMA, BAND>, a, sa, fmap,
+                              c->state_map[parity]);
 }
 
 template <int N, int BPT, int MINB, bool FTMA>
 cudaError_t setup_staged(dmsgm_ctx* c) {
-    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, FTMA>,
+    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, FTMA, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, FTMA>,
+        e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, FTMA, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
+    if constexpr (MINB == 3 && FTMA) {   // the band-mode variants (default configuration only)
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, FTMA, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, FTMA, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
+    }
     if (e != cudaSuccess) return e;
     int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB, false, FTMA>,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB, false, FTMA, false>,
                                                       kStagedThreads, Staged<N, BPT, FTMA>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -256,12 +275,12 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
                         cudaStream_t stream) {
     StepArgs a;
     a.frames = frames;
-    a.fstride = (long long)c->H * (long long)fpitch;
+    a.fstride = (long long)c->Hp * (long long)fpitch;
     a.fpitch = (int)fpitch;
     a.mpitch = (int)mpitch;
     a.H = H;
     a.masks = masks;
-    a.mstride = (long long)c->H * (long long)mpitch;
+    a.mstride = (long long)c->Hp * (long long)mpitch;
     const size_t sstride = stream_floats(c);
     a.prev = c->state[parity] + (size_t)s0 * sstride;
     a.next = c->state[parity ^ 1] + (size_t)s0 * sstride;
@@ -269,6 +288,14 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     a.fresh_out = c->fresh[parity ^ 1] + s0;
     a.Wb = c->Wb;
     a.Hb = c->Hb;
+    a.row0 = c->row0;
+    a.rows = c->rows;
+    a.lo = c->band ? (c->row0 - c->halo > 0 ? c->row0 - c->halo : 0) : 0;
+    a.hi = c->band ? (c->row0 + c->rows + c->halo < c->Hb ? c->row0 + c->rows + c->halo : c->Hb) : c->Hb;
+    a.halo = c->halo;
+    a.peer_up = c->peer_state[0][parity ^ 1] ? c->peer_state[0][parity ^ 1] + (size_t)s0 * sstride : nullptr;
+    a.peer_dn = c->peer_state[1][parity ^ 1] ? c->peer_state[1][parity ^ 1] + (size_t)s0 * sstride : nullptr;
+    a.status = c->status_dev;
     const int bpt = bpt_of(c);
     a.Wstrips = c->Wb / bpt;
     a.tiles_x = tiles_x_of(c);
@@ -276,12 +303,19 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     a.kp = kparams(c->p);
     dim3 block(kCtaX, kCtaY, 1);
     // each CTA walks kRowsPerCta tile rows of one stream (prefetching the next one)
-    const int tiles_y = (c->Hb + kCtaY - 1) / kCtaY;
+    const int tiles_y = (c->rows + kCtaY - 1) / kCtaY;
     dim3 grid((a.Wstrips + kCtaX - 1) / kCtaX, (tiles_y + kRowsPerCta - 1) / kRowsPerCta, count);
     if (c->staged) {
         // RULES = the App. E compatibility switches (R27/R28) are on: runtime-switched code;
         // otherwise the default rules are compiled in without branches.
         const bool rules = c->p.update_rule != 0 || c->p.classify_rule != 0;
+        if (c->band) {   // band mode: halo check + neighbour stores compiled in
+            if (c->N == 4)
+                return rules ? launch_staged<4, 2, 3, true, true, true>(c, a, frames, fpitch, s0, count, parity, stream)
+                             : launch_staged<4, 2, 3, false, true, true>(c, a, frames, fpitch, s0, count, parity, stream);
+            return rules ? launch_staged<8, 1, 3, true, true, true>(c, a, frames, fpitch, s0, count, parity, stream)
+                         : launch_staged<8, 1, 3, false, true, true>(c, a, frames, fpitch, s0, count, parity, stream);
+        }
 #define DMSGM_STAGED(NN, BB, OO, FT)                                                                        \
     return rules ? launch_staged<NN, BB, OO, true, FT>(c, a, frames, fpitch, s0, count, parity, stream)    \
                  : launch_staged<NN, BB, OO, false, FT>(c, a, frames, fpitch, s0, count, parity, stream)
@@ -319,8 +353,33 @@ int check_images(dmsgm_ctx* c, const void* frames, size_t fpitch, const void* H,
     if ((uintptr_t)H & 7) return fail(c, DMSGM_EINVAL, "homographies must be 8-byte aligned");
     if (fpitch < (size_t)c->W || (fpitch & 15)) return fail(c, DMSGM_EINVAL, "frame_pitch must be >= width and a multiple of 16");
     if (mpitch < (size_t)c->W || (mpitch & 15)) return fail(c, DMSGM_EINVAL, "mask_pitch must be >= width and a multiple of 16");
-    if ((double)fpitch * c->H > 2147483647.0 || (double)mpitch * c->H > 2147483647.0)
+    if ((double)fpitch * c->Hp > 2147483647.0 || (double)mpitch * c->Hp > 2147483647.0)
         return fail(c, DMSGM_EINVAL, "one image (pitch x height) must be < 2 GiB");
+    return DMSGM_OK;
+}
+
+bool has_peers(const dmsgm_ctx* c) { return c->peer_slot[0] || c->peer_slot[1]; }
+
+// Enqueue the band signal / wait kernel (one thread).
+cudaError_t launch_sync(dmsgm_ctx* c, int signal, int wait, cudaStream_t stream) {
+    SyncArgs sa;
+    sa.flags = c->flags;
+    sa.peer_slot[0] = c->peer_slot[0];
+    sa.peer_slot[1] = c->peer_slot[1];
+    sa.signal = signal;
+    sa.wait = wait;
+    const char* tenv = getenv("DMSGM_BAND_TIMEOUT_MS");
+    sa.timeout_ns = (unsigned long long)(tenv ? atof(tenv) : 10000.0) * 1000000ull;
+    sa.status = c->status_dev;
+    dmsgm_band_sync_kernel<<<1, 32, 0, stream>>>(sa);
+    return cudaGetLastError();
+}
+
+// A halo overflow / peer timeout recorded by an earlier step (host-mapped word, no sync).
+int check_status(dmsgm_ctx* c) {
+    const unsigned st = c->status_host ? *(volatile unsigned*)c->status_host : 0u;
+    if (st & 1u) return fail(c, DMSGM_ESTATE, "row band: a source block lay outside the band's halo (halo too small)");
+    if (st & 2u) return fail(c, DMSGM_ECUDA, "row band: timed out waiting for a neighbour's step");
     return DMSGM_OK;
 }
 
@@ -362,6 +421,7 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
     c->W = width; c->H = height; c->N = block;
     c->Wb = width / block; c->Hb = height / block;
     c->S = p->num_streams; c->device = device; c->p = *p;
+    c->band = 0; c->row0 = 0; c->rows = c->Hb; c->halo = 0; c->Hp = c->H;
     const size_t sbytes = (size_t)c->S * stream_floats(c) * sizeof(float);
     for (int i = 0; i < 2; ++i) {
         if ((e = cudaMalloc(&c->state[i], sbytes)) != cudaSuccess ||
@@ -393,7 +453,15 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
             c->staged = 1;
         }
     }
-    if ((e = cudaMemset(c->state[0], 0, sbytes)) != cudaSuccess ||
+    if ((e = cudaMalloc(&c->flags, 3 * sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaHostAlloc(&c->status_host, sizeof(unsigned), cudaHostAllocMapped)) != cudaSuccess ||
+        (e = cudaHostGetDevicePointer(&c->status_dev, c->status_host, 0)) != cudaSuccess) {
+        dmsgm_destroy(c);
+        return fail(nullptr, DMSGM_ENOMEM, "flag allocation failed: %s", cudaGetErrorString(e));
+    }
+    *c->status_host = 0;
+    if ((e = cudaMemset(c->flags, 0, 3 * sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMemset(c->state[0], 0, sbytes)) != cudaSuccess ||
         (e = cudaMemset(c->state[1], 0, sbytes)) != cudaSuccess ||
         (e = cudaMemset(c->fresh[0], 1, (size_t)c->S)) != cudaSuccess ||
         (e = cudaMemset(c->fresh[1], 1, (size_t)c->S)) != cudaSuccess ||
@@ -411,12 +479,14 @@ int dmsgm_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, const double*
     if (!c) return DMSGM_EINVAL;
     int rc = check_images(c, frames, fpitch, H, masks, mpitch);
     if (rc) return rc;
+    if ((rc = check_status(c))) return rc;
     DeviceGuard g(c->device);
     if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
     cudaError_t e = launch_step(c, frames, fpitch, H, masks, mpitch, 0, c->S, c->cur,
                                 (cudaStream_t)cuda_stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_step launch");
     c->cur ^= 1;
+    c->steps += 1;
     return DMSGM_OK;
 }
 
@@ -426,9 +496,10 @@ int dmsgm_step_n(dmsgm_ctx* c, int T, const uint8_t* frames, size_t fpitch, cons
     if (T < 1) return fail(c, DMSGM_EINVAL, "T must be >= 1");
     int rc = check_images(c, frames, fpitch, H, masks, mpitch);
     if (rc) return rc;
+    if ((rc = check_status(c))) return rc;
     DeviceGuard g(c->device);
     if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
-    const size_t fframe = (size_t)c->S * c->H * fpitch, mframe = (size_t)c->S * c->H * mpitch;
+    const size_t fframe = (size_t)c->S * c->Hp * fpitch, mframe = (size_t)c->S * c->Hp * mpitch;
     GraphSlot* slot = nullptr;
     for (auto& gs : c->graphs)
         if (gs.valid && gs.T == T && gs.parity == c->cur && gs.frames == frames && gs.H == H &&
@@ -448,6 +519,8 @@ int dmsgm_step_n(dmsgm_ctx* c, int T, const uint8_t* frames, size_t fpitch, cons
         for (int t = 0; t < T && le == cudaSuccess; ++t) {
             le = launch_step(c, frames + t * fframe, fpitch, H + (size_t)t * c->S * 9, masks + t * mframe,
                              mpitch, 0, c->S, parity, c->capture_stream);
+            // band mode with neighbours: every step ends with the signal / wait exchange
+            if (le == cudaSuccess && has_peers(c)) le = launch_sync(c, 1, 1, c->capture_stream);
             parity ^= 1;
         }
         e = cudaStreamEndCapture(c->capture_stream, &graph);
@@ -463,6 +536,7 @@ int dmsgm_step_n(dmsgm_ctx* c, int T, const uint8_t* frames, size_t fpitch, cons
     e = cudaGraphLaunch(slot->exec, (cudaStream_t)cuda_stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphLaunch");
     if (T & 1) c->cur ^= 1;
+    c->steps += (unsigned)T;
     return DMSGM_OK;
 }
 
@@ -476,7 +550,9 @@ int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double
     if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
     cudaError_t e;
     const size_t dpitch = ((size_t)c->W + 15) & ~(size_t)15;
-    const size_t fimg = (size_t)c->H * dpitch;
+    const size_t fimg = (size_t)c->Hp * dpitch;
+    int rc = check_status(c);
+    if (rc) return rc;
     if (!c->pipe_ready) {
         const size_t nb = (size_t)c->S * fimg;
         if ((e = cudaMalloc(&c->st_frames, nb)) != cudaSuccess || (e = cudaMalloc(&c->st_masks, nb)) != cudaSuccess ||
@@ -501,7 +577,7 @@ int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double
         cudaStream_t st = c->pipe[k % kPipeStreams];
         uint8_t* df = c->st_frames + (size_t)s0 * fimg;
         uint8_t* dm = c->st_masks + (size_t)s0 * fimg;
-        if ((e = cudaMemcpy2DAsync(df, dpitch, hf + (size_t)s0 * c->H * fpitch, fpitch, c->W, (size_t)cnt * c->H,
+        if ((e = cudaMemcpy2DAsync(df, dpitch, hf + (size_t)s0 * c->Hp * fpitch, fpitch, c->W, (size_t)cnt * c->Hp,
                                    cudaMemcpyHostToDevice, st)) != cudaSuccess)
             return cuda_fail(c, e, "H2D frames");
         if ((e = cudaMemcpyAsync(c->st_H + (size_t)s0 * 9, hH + (size_t)s0 * 9, (size_t)cnt * 9 * sizeof(double),
@@ -509,13 +585,14 @@ int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double
             return cuda_fail(c, e, "H2D homographies");
         if ((e = launch_step(c, df, dpitch, c->st_H + (size_t)s0 * 9, dm, dpitch, s0, cnt, parity, st)) != cudaSuccess)
             return cuda_fail(c, e, "dmsgm_step_host launch");
-        if ((e = cudaMemcpy2DAsync(hm + (size_t)s0 * c->H * mpitch, mpitch, dm, dpitch, c->W, (size_t)cnt * c->H,
+        if ((e = cudaMemcpy2DAsync(hm + (size_t)s0 * c->Hp * mpitch, mpitch, dm, dpitch, c->W, (size_t)cnt * c->Hp,
                                    cudaMemcpyDeviceToHost, st)) != cudaSuccess)
             return cuda_fail(c, e, "D2H masks");
     }
     for (int i = 0; i < kPipeStreams; ++i)
         if ((e = cudaStreamSynchronize(c->pipe[i])) != cudaSuccess) return cuda_fail(c, e, "dmsgm_step_host sync");
     c->cur ^= 1;
+    c->steps += 1;
     return DMSGM_OK;
 }
 
@@ -591,15 +668,226 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     if (!c || !out) return DMSGM_EINVAL;
     out->width = c->W; out->height = c->H; out->block = c->N;
     out->blocks_x = c->Wb; out->blocks_y = c->Hb; out->num_streams = c->S;
-    out->kernels_per_step = 1;
+    out->kernels_per_step = has_peers(c) ? 2 : 1;
+    out->band_row0 = c->row0; out->band_rows = c->rows; out->band_halo = c->halo;
     out->state_bytes = (size_t)c->S * stream_floats(c) * sizeof(float);
     // frame read (1 B/px) + mask write (1 B/px) + state read + write (2 x 24 B per block)
-    out->algorithmic_bytes_per_frame = 2.0 * c->W * c->H + 2.0 * 24.0 * (double)plane_elems(c);
+    // (band mode: the band's rows, plus the halo rows stored into each neighbour)
+    const int nb = (c->peer_slot[0] ? 1 : 0) + (c->peer_slot[1] ? 1 : 0);
+    out->algorithmic_bytes_per_frame = 2.0 * c->W * c->Hp + 2.0 * 24.0 * (double)c->Wb * c->rows +
+                                       24.0 * (double)c->Wb * c->halo * nb;
     if (c->staged)
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d,%s> (TMA, persistent)", c->N,
                  c->N == 4 ? 2 : 1, c->staged_occ, c->staged_ftma ? "frames:tma" : "frames:regs");
     else
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_kernel<%d,%d>", c->N, bpt_of(c));
+    if (c->staged && c->band)
+        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,3,frames:tma,band> (TMA, persistent)",
+                 c->N, c->N == 4 ? 2 : 1);
+    return DMSGM_OK;
+}
+
+// ---- row band ----
+
+namespace {
+void detach(dmsgm_ctx* c, int side) {
+    for (int k = 0; k < 3; ++k)
+        if (c->ipc_open[side][k]) {
+            cudaIpcCloseMemHandle(c->ipc_open[side][k]);
+            c->ipc_open[side][k] = nullptr;
+        }
+    c->peer_state[side][0] = c->peer_state[side][1] = nullptr;
+    c->peer_slot[side] = nullptr;
+}
+
+int band_side_ok(dmsgm_ctx* c, int side) {
+    if (side != 0 && side != 1) return fail(c, DMSGM_EINVAL, "side must be 0 (above) or 1 (below)");
+    if (!c->band) return fail(c, DMSGM_ESTATE, "dmsgm_set_band first");
+    if (side == 0 && c->row0 == 0) return fail(c, DMSGM_ESTATE, "the band starts at row 0: no band above");
+    if (side == 1 && c->row0 + c->rows == c->Hb) return fail(c, DMSGM_ESTATE, "the band ends at the last row: no band below");
+    if (c->halo < 1) return fail(c, DMSGM_ESTATE, "a band with neighbours needs halo >= 1");
+    return DMSGM_OK;
+}
+}  // namespace
+
+int dmsgm_set_band(dmsgm_ctx* c, int row0, int rows, int halo) {
+    if (!c) return DMSGM_EINVAL;
+    if (row0 < 0 || rows < 1 || row0 + rows > c->Hb)
+        return fail(c, DMSGM_EINVAL, "band rows [%d, %d) outside [0, %d)", row0, row0 + rows, c->Hb);
+    if (halo < 0 || halo > rows) return fail(c, DMSGM_EINVAL, "halo must be in [0, rows]");
+    DeviceGuard g(c->device);
+    if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_set_band sync");
+    destroy_graphs(c);
+    detach(c, 0);
+    detach(c, 1);
+    const bool whole = row0 == 0 && rows == c->Hb && halo == 0;
+    if (!whole && c->staged && (c->staged_occ != 3 || !c->staged_ftma)) {
+        // the band kernels exist in the default configuration only
+        e = c->N == 4 ? setup_staged<4, 2, 3, true>(c) : setup_staged<8, 1, 3, true>(c);
+        if (e != cudaSuccess) return cuda_fail(c, e, "band kernel setup");
+        c->staged_occ = 3;
+        c->staged_ftma = 1;
+    }
+    c->band = whole ? 0 : 1;
+    c->row0 = row0;
+    c->rows = rows;
+    c->halo = halo;
+    c->Hp = rows * c->N;
+    c->steps = 0;
+    *c->status_host = 0;
+    if ((e = cudaMemset(c->flags, 0, 3 * sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMemset(c->fresh[0], 1, (size_t)c->S)) != cudaSuccess ||
+        (e = cudaMemset(c->fresh[1], 1, (size_t)c->S)) != cudaSuccess ||
+        (e = cudaDeviceSynchronize()) != cudaSuccess)
+        return cuda_fail(c, e, "dmsgm_set_band reset");
+    return DMSGM_OK;
+}
+
+int dmsgm_get_buffers(const dmsgm_ctx* c, dmsgm_buffers* out) {
+    if (!c || !out) return DMSGM_EINVAL;
+    out->state[0] = c->state[0];
+    out->state[1] = c->state[1];
+    out->flags = c->flags;
+    out->parity = c->cur;
+    out->steps = c->steps;
+    out->row_bytes = (size_t)tiles_x_of(c) * kTileFloats * sizeof(float);
+    out->stream_bytes = stream_floats(c) * sizeof(float);
+    return DMSGM_OK;
+}
+
+int dmsgm_attach_peer(dmsgm_ctx* c, int side, const dmsgm_buffers* p) {
+    if (!c) return DMSGM_EINVAL;
+    int rc = band_side_ok(c, side);
+    if (rc) return rc;
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_attach_peer sync");
+    destroy_graphs(c);
+    detach(c, side);
+    if (!p) return DMSGM_OK;
+    if (!p->state[0] || !p->state[1] || !p->flags) return fail(c, DMSGM_EINVAL, "null peer buffer");
+    if (p->stream_bytes != stream_floats(c) * sizeof(float))
+        return fail(c, DMSGM_EINVAL, "peer state size differs (width/block/height mismatch)");
+    if (p->parity != c->cur || p->steps != c->steps)
+        return fail(c, DMSGM_ESTATE, "peer is not in lockstep (parity %d/%d, steps %u/%u)", p->parity, c->cur,
+                    p->steps, c->steps);
+    c->peer_state[side][0] = (float*)p->state[0];
+    c->peer_state[side][1] = (float*)p->state[1];
+    // the neighbour above listens on its flags[1] ("from below"), the one below on flags[0]
+    c->peer_slot[side] = (unsigned*)p->flags + (side == 0 ? 1 : 0);
+    return DMSGM_OK;
+}
+
+int dmsgm_get_ipc_handles(const dmsgm_ctx* c, void* out, size_t n) {
+    if (!c || !out || n < DMSGM_IPC_BYTES) return DMSGM_EINVAL;
+    static_assert(3 * sizeof(cudaIpcMemHandle_t) <= DMSGM_IPC_BYTES, "IPC handle size");
+    DeviceGuard g(c->device);
+    cudaIpcMemHandle_t h[3];
+    cudaError_t e;
+    if ((e = cudaIpcGetMemHandle(&h[0], c->state[0])) != cudaSuccess ||
+        (e = cudaIpcGetMemHandle(&h[1], c->state[1])) != cudaSuccess ||
+        (e = cudaIpcGetMemHandle(&h[2], c->flags)) != cudaSuccess)
+        return cuda_fail(const_cast<dmsgm_ctx*>(c), e, "cudaIpcGetMemHandle");
+    memset(out, 0, DMSGM_IPC_BYTES);
+    memcpy(out, h, sizeof h);
+    return DMSGM_OK;
+}
+
+int dmsgm_attach_peer_ipc(dmsgm_ctx* c, int side, const void* handles, size_t n) {
+    if (!c) return DMSGM_EINVAL;
+    if (!handles || n < DMSGM_IPC_BYTES) return fail(c, DMSGM_EINVAL, "need %d bytes of handles", DMSGM_IPC_BYTES);
+    int rc = band_side_ok(c, side);
+    if (rc) return rc;
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_attach_peer_ipc sync");
+    destroy_graphs(c);
+    detach(c, side);
+    cudaIpcMemHandle_t h[3];
+    memcpy(h, handles, sizeof h);
+    for (int k = 0; k < 3; ++k) {
+        if ((e = cudaIpcOpenMemHandle(&c->ipc_open[side][k], h[k], cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess) {
+            detach(c, side);
+            return cuda_fail(c, e, "cudaIpcOpenMemHandle");
+        }
+    }
+    c->peer_state[side][0] = (float*)c->ipc_open[side][0];
+    c->peer_state[side][1] = (float*)c->ipc_open[side][1];
+    c->peer_slot[side] = (unsigned*)c->ipc_open[side][2] + (side == 0 ? 1 : 0);
+    return DMSGM_OK;
+}
+
+namespace {
+int band_sync_common(dmsgm_ctx* c, int signal, int wait, void* stream, const char* what) {
+    if (!c) return DMSGM_EINVAL;
+    if (!c->band) return fail(c, DMSGM_ESTATE, "%s: dmsgm_set_band first", what);
+    DeviceGuard g(c->device);
+    if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
+    if (!has_peers(c)) return DMSGM_OK;   // a lone band: nothing to exchange
+    cudaError_t e = launch_sync(c, signal, wait, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, what);
+    return DMSGM_OK;
+}
+}  // namespace
+
+int dmsgm_band_signal(dmsgm_ctx* c, void* s) { return band_sync_common(c, 1, 0, s, "dmsgm_band_signal"); }
+int dmsgm_band_wait(dmsgm_ctx* c, void* s) { return band_sync_common(c, 0, 1, s, "dmsgm_band_wait"); }
+int dmsgm_band_sync(dmsgm_ctx* c, void* s) { return band_sync_common(c, 1, 1, s, "dmsgm_band_sync"); }
+
+int dmsgm_get_status(dmsgm_ctx* c, unsigned* out) {
+    if (!c || !out) return DMSGM_EINVAL;
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_get_status sync");
+    *out = *(volatile unsigned*)c->status_host;
+    *(volatile unsigned*)c->status_host = 0;
+    return DMSGM_OK;
+}
+
+int dmsgm_band_halo_needed(int width, int height, int block, const double* H, int count, int row0, int rows,
+                           int* out) {
+    if (!H || !out || count < 1 || block < 1 || width <= 0 || height <= 0 || width % block || height % block)
+        return DMSGM_EINVAL;
+    const int N = block, Wb = width / N, Hb = height / N;
+    if (row0 < 0 || rows < 1 || row0 + rows > Hb) return DMSGM_EINVAL;
+    int need = 0;
+    for (int s = 0; s < count; ++s) {
+        const double* h = H + 9 * s;
+        // S1 as the kernel computes it (R17: fp32 displacement form, explicit fma)
+        float gg[9];
+        for (int j = 0; j < 9; ++j) gg[j] = (float)((j == 0 || j == 4 || j == 8) ? h[j] - 1.0 : h[j]);
+        for (int bj = row0; bj < row0 + rows; ++bj) {
+            const float Y = (float)(N * bj) + 0.5f * (float)N;
+            const float r7 = fmaf(gg[7], Y, gg[8]), r1 = fmaf(gg[1], Y, gg[2]), r4 = fmaf(gg[4], Y, gg[5]);
+            for (int bi = 0; bi < Wb; ++bi) {
+                const float X = (float)(N * bi) + 0.5f * (float)N;
+                const float e = fmaf(gg[6], X, r7);
+                const float w = 1.0f + e;
+                if (!(w > 0.0f)) continue;
+                const float px = fmaf(-X, e, fmaf(gg[0], X, r1));
+                const float py = fmaf(-Y, e, fmaf(gg[3], X, r4));
+                const float rwN = (1.0f / w) * (1.0f / (float)N);
+                const float ex = px * rwN, ey = py * rwN;
+                if (!(fabsf(ex) < 1048576.0f && fabsf(ey) < 1048576.0f)) continue;
+                const float tx = 0.5f + ex, ty = 0.5f + ey;
+                const float fxf = floorf(tx), fyf = floorf(ty);
+                const float du = (tx - fxf) - 0.5f, dv = (ty - fyf) - 0.5f;
+                const int iu = bi + (int)fxf, iv = bj + (int)fyf;
+                const int ju = du > 0.0f ? iu + 1 : iu - 1, jv = dv > 0.0f ? iv + 1 : iv - 1;
+                const float a = fabsf(du), b = fabsf(dv);
+                const float wt[4] = {(1.0f - a) * (1.0f - b), a * (1.0f - b), (1.0f - a) * b, a * b};
+                const int cxs[4] = {iu, ju, iu, ju}, cys[4] = {iv, iv, jv, jv};
+                for (int k = 0; k < 4; ++k) {
+                    if (!(wt[k] > 0.0f) || cxs[k] < 0 || cxs[k] >= Wb || cys[k] < 0 || cys[k] >= Hb) continue;
+                    const int d = cys[k] < row0 ? row0 - cys[k] : (cys[k] >= row0 + rows ? cys[k] - (row0 + rows - 1) : 0);
+                    if (d > need) need = d;
+                }
+            }
+        }
+    }
+    *out = need;
     return DMSGM_OK;
 }
 
@@ -610,6 +898,11 @@ void dmsgm_destroy(dmsgm_ctx* c) {
     DeviceGuard g(c->device);
     cudaDeviceSynchronize();
     destroy_graphs(c);
+    for (int side = 0; side < 2; ++side)
+        for (int k = 0; k < 3; ++k)
+            if (c->ipc_open[side][k]) cudaIpcCloseMemHandle(c->ipc_open[side][k]);
+    if (c->flags) cudaFree(c->flags);
+    if (c->status_host) cudaFreeHost(c->status_host);
     for (int i = 0; i < 2; ++i) {
         if (c->state[i]) cudaFree(c->state[i]);
         if (c->fresh[i]) cudaFree(c->fresh[i]);

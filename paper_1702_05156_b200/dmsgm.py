@@ -27,7 +27,11 @@ _ERRNAMES = {-1: "DMSGM_EINVAL", -2: "DMSGM_ENOMEM", -3: "DMSGM_ECUDA", -4: "DMS
 # Every symbol include/dmsgm.h declares (checked by tests/test_abi.py).
 EXPORTS = ("dmsgm_create", "dmsgm_step", "dmsgm_step_n", "dmsgm_step_host", "dmsgm_reset",
            "dmsgm_get_state", "dmsgm_set_state", "dmsgm_is_initialised", "dmsgm_get_info",
-           "dmsgm_last_error", "dmsgm_destroy", "dmsgm_version")
+           "dmsgm_last_error", "dmsgm_destroy", "dmsgm_version",
+           "dmsgm_set_band", "dmsgm_get_buffers", "dmsgm_attach_peer", "dmsgm_get_ipc_handles",
+           "dmsgm_attach_peer_ipc", "dmsgm_band_signal", "dmsgm_band_wait", "dmsgm_band_sync",
+           "dmsgm_get_status", "dmsgm_band_halo_needed")
+DMSGM_IPC_BYTES = 192
 
 
 class DmsgmError(RuntimeError):
@@ -49,8 +53,14 @@ class dmsgm_info(ctypes.Structure):
     _fields_ = [("width", ctypes.c_int), ("height", ctypes.c_int), ("block", ctypes.c_int),
                 ("blocks_x", ctypes.c_int), ("blocks_y", ctypes.c_int),
                 ("num_streams", ctypes.c_int), ("kernels_per_step", ctypes.c_int),
+                ("band_row0", ctypes.c_int), ("band_rows", ctypes.c_int), ("band_halo", ctypes.c_int),
                 ("state_bytes", ctypes.c_size_t), ("algorithmic_bytes_per_frame", ctypes.c_double),
                 ("kernel", ctypes.c_char * 64)]
+
+
+class dmsgm_buffers(ctypes.Structure):
+    _fields_ = [("state", ctypes.c_void_p * 2), ("flags", ctypes.c_void_p), ("parity", ctypes.c_int),
+                ("steps", ctypes.c_uint), ("row_bytes", ctypes.c_size_t), ("stream_bytes", ctypes.c_size_t)]
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -72,6 +82,16 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.dmsgm_last_error.restype = ctypes.c_char_p
     lib.dmsgm_destroy.argtypes = [P]
     lib.dmsgm_destroy.restype = None
+    lib.dmsgm_set_band.argtypes = [P, i32, i32, i32]
+    lib.dmsgm_get_buffers.argtypes = [P, ctypes.POINTER(dmsgm_buffers)]
+    lib.dmsgm_attach_peer.argtypes = [P, i32, ctypes.POINTER(dmsgm_buffers)]
+    lib.dmsgm_get_ipc_handles.argtypes = [P, P, sz]
+    lib.dmsgm_attach_peer_ipc.argtypes = [P, i32, P, sz]
+    lib.dmsgm_band_signal.argtypes = [P, P]
+    lib.dmsgm_band_wait.argtypes = [P, P]
+    lib.dmsgm_band_sync.argtypes = [P, P]
+    lib.dmsgm_get_status.argtypes = [P, ctypes.POINTER(ctypes.c_uint)]
+    lib.dmsgm_band_halo_needed.argtypes = [i32, i32, i32, P, i32, i32, i32, ctypes.POINTER(ctypes.c_int)]
     lib.dmsgm_version.argtypes = []
     lib.dmsgm_version.restype = ctypes.c_char_p
     return lib
@@ -202,6 +222,58 @@ class Dmsgm:
         info = dmsgm_info()
         self._check(self._lib.dmsgm_get_info(self._h, ctypes.byref(info)))
         return info
+
+    # -- row band (include/dmsgm.h) -------------------------------
+    def set_band(self, row0: int, rows: int, halo: int):
+        self._check(self._lib.dmsgm_set_band(self._h, row0, rows, halo))
+        self.info = self.get_info()
+
+    def get_buffers(self) -> dmsgm_buffers:
+        b = dmsgm_buffers()
+        self._check(self._lib.dmsgm_get_buffers(self._h, ctypes.byref(b)))
+        return b
+
+    def attach_peer(self, side: int, peer: "Dmsgm | dmsgm_buffers | None"):
+        if peer is None:
+            self._check(self._lib.dmsgm_attach_peer(self._h, side, None))
+        else:
+            b = peer.get_buffers() if isinstance(peer, Dmsgm) else peer
+            self._check(self._lib.dmsgm_attach_peer(self._h, side, ctypes.byref(b)))
+        self.info = self.get_info()
+
+    def get_ipc_handles(self) -> bytes:
+        buf = ctypes.create_string_buffer(DMSGM_IPC_BYTES)
+        self._check(self._lib.dmsgm_get_ipc_handles(self._h, buf, DMSGM_IPC_BYTES))
+        return buf.raw
+
+    def attach_peer_ipc(self, side: int, handles: bytes):
+        buf = ctypes.create_string_buffer(bytes(handles), len(handles))
+        self._check(self._lib.dmsgm_attach_peer_ipc(self._h, side, buf, len(handles)))
+        self.info = self.get_info()
+
+    def band_signal(self, stream=None):
+        self._check(self._lib.dmsgm_band_signal(self._h, _stream_handle(stream)))
+
+    def band_wait(self, stream=None):
+        self._check(self._lib.dmsgm_band_wait(self._h, _stream_handle(stream)))
+
+    def band_sync(self, stream=None):
+        self._check(self._lib.dmsgm_band_sync(self._h, _stream_handle(stream)))
+
+    def get_status(self) -> int:
+        v = ctypes.c_uint(0)
+        self._check(self._lib.dmsgm_get_status(self._h, ctypes.byref(v)))
+        return v.value
+
+
+def band_halo_needed(width: int, height: int, block: int, homographies: np.ndarray, row0: int, rows: int) -> int:
+    """Halo rows band [row0, row0+rows) needs for HOST homographies f64 [count][9]."""
+    H = np.ascontiguousarray(homographies, np.float64).reshape(-1, 9)
+    out = ctypes.c_int(0)
+    rc = _lib.dmsgm_band_halo_needed(width, height, block, _ptr(H), H.shape[0], row0, rows, ctypes.byref(out))
+    if rc != DMSGM_OK:
+        raise DmsgmError(rc, "dmsgm_band_halo_needed: bad arguments")
+    return out.value
 
 
 def version() -> str:
