@@ -380,10 +380,16 @@ def run_band(args, rank, world, local):
     from paper_1702_05156_b200.band import BandGroup, BandRank, band_rows, halo_for
     from paper_1702_05156_b200.shard import max_over_ranks
 
+    if args.same_device:          # functional check of the torchrun path on a 1-GPU box
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
+    red_dev = dev if args.dist_backend == "nccl" else None
     wl = WORKLOADS[args.config]
     cfg = synth.config(wl["ring"])
     W, H, N = cfg.W, cfg.H, cfg.N
@@ -394,26 +400,33 @@ def run_band(args, rank, world, local):
     frames, Hs = synth.generate_device(cfg, T=RING, device=f"cuda:{local}")    # [R][1][H][W]
     Hs_dev = torch.from_numpy(np.ascontiguousarray(Hs)).to(dev)
     halo = halo_for(W, H, N, Hs.reshape(-1, 9), bands)
-    masks = torch.empty_like(frames)
     params = method_params(dm, 1)
     main_stream = torch.cuda.current_stream(dev)
     if world > 1:
         br = BandRank(W, H, N, params, rank, world, halo, device=local, exchange=args.exchange)
         ctxs, my_bands = [br.ctx], [br.band]
-        sl = slice(br.band.row0 * N, br.band.row1 * N)
         streams = [main_stream]
-
-        def step(i):
-            r = i % RING
-            br.step(frames[r][:, sl], Hs_dev[r], masks[r][:, sl])
     else:
         streams = [torch.cuda.Stream(dev) for _ in range(G)] if G > 1 else [main_stream]
         grp = BandGroup(W, H, N, params, G, halo, device=local, streams=streams if G > 1 else None)
         ctxs, my_bands = grp.ctxs, grp.bands
+    # per-band rings [R][1][rows*N][W] (a band's images are contiguous per frame)
+    fb = [frames[:, :, b.row0 * N:b.row1 * N].contiguous() for b in my_bands]
+    mb = [torch.empty_like(f) for f in fb]
+    del frames
 
-        def step(i):
-            r = i % RING
-            grp.step(frames[r], Hs_dev[r], masks[r])
+    def launch(T):
+        """T consecutive frames of the ring as one CUDA graph per band (step + sync per frame)."""
+        if world > 1:
+            br.step_n(T, fb[0], Hs_dev[:T], mb[0])
+        else:
+            grp.step_n(T, fb, Hs_dev[:T], mb)
+
+    def run_steps(n):
+        for _ in range(n // RING):
+            launch(RING)
+        if n % RING:
+            launch(n % RING)
     bytes_per_step = sum(c.info.algorithmic_bytes_per_frame for c in ctxs)
     launches_per_step = sum(c.info.kernels_per_step for c in ctxs)
     kernel_name = ctxs[0].info.kernel.decode()
@@ -428,9 +441,15 @@ def run_band(args, rank, world, local):
             if st is not main_stream:
                 main_stream.wait_stream(st)
 
+    # warm-up: capture (and run) the graphs the timed region replays
+    warm = 0
     fork()
-    for i in range(args.warmup):
-        step(i)
+    while warm < args.warmup:
+        launch(RING)
+        warm += RING
+    if args.steps % RING:
+        launch(args.steps % RING)
+        warm += args.steps % RING
     join()
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -443,8 +462,7 @@ def run_band(args, rank, world, local):
         torch.cuda.nvtx.range_push("timed")
         ev0.record(main_stream)
         fork()
-        for i in range(args.steps):
-            step(args.warmup + i)
+        run_steps(args.steps)
         join()
         ev1.record(main_stream)
         torch.cuda.nvtx.range_pop()
@@ -454,7 +472,7 @@ def run_band(args, rank, world, local):
     if world > 1:
         dist.barrier()
     ms_local = ev0.elapsed_time(ev1)
-    ms = max_over_ranks(ms_local, dev)
+    ms = max_over_ranks(ms_local, red_dev)
     fps = args.steps / (ms / 1e3)
     peak, peak_src = measured_peak()
     achieved = bytes_per_step / (ms_local / args.steps / 1e3) / 1e9
@@ -464,17 +482,23 @@ def run_band(args, rank, world, local):
     e2e = None
     if not args.no_e2e:
         y0, y1 = my_bands[0].row0 * N, my_bands[-1].row1 * N
-        hf = [frames[r][:, y0:y1].cpu().pin_memory() for r in range(2)]
-        hm = torch.empty((1, y1 - y0, W), dtype=torch.uint8, pin_memory=True)
+        hf = [[f[r].cpu().pin_memory() for f in fb] for r in range(2)]
+        hm = [torch.empty_like(m[0], device="cpu").pin_memory() for m in mb]
         e2e_steps = max(3, min(args.steps, args.e2e_steps))
 
         def e2e_step(i):
+            # this step's frame rows: pinned host -> device, one step of every band, masks -> host
             r = i % 2
-            frames[r][:, y0:y1].copy_(hf[r], non_blocking=True)
+            for f, h in zip(fb, hf[r]):
+                f[r].copy_(h, non_blocking=True)
             fork()
-            step(r)
+            if world > 1:
+                br.step(fb[0][r], Hs_dev[r], mb[0][r])
+            else:
+                grp.step([f[r] for f in fb], Hs_dev[r], [m[r] for m in mb])
             join()
-            hm.copy_(masks[r][:, y0:y1], non_blocking=True)
+            for m, h in zip(mb, hm):
+                h.copy_(m[r], non_blocking=True)
             torch.cuda.synchronize(dev)
         for i in range(3):
             e2e_step(i)
@@ -483,17 +507,17 @@ def run_band(args, rank, world, local):
         t0 = time.perf_counter()
         for i in range(e2e_steps):
             e2e_step(i)
-        e2e_s = max_over_ranks(time.perf_counter() - t0, dev)
+        e2e_s = max_over_ranks(time.perf_counter() - t0, red_dev)
         e2e = {"value": e2e_steps / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": (y1 - y0) * W,
                "d2h_bytes_per_step": (y1 - y0) * W, "steps": e2e_steps,
                "api": "band step (BandGroup/BandRank.step) between pinned-host copies, synchronous"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        fh = frames[:2].cpu().numpy()
+        seq = synth.generate(cfg, T=2)
         per_frame = 0.021 * (W * H) / (1920 * 1080)
         nf = max(2, int(args.cpu_seconds / per_frame))
-        cfps, used, wall = oracle_throughput(cfg, fh, Hs[:2], 1, nf, 1)
+        cfps, used, wall = oracle_throughput(cfg, seq.frames, seq.homographies, 1, nf, 1)
         cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle",
                "sample": f"1 stream x {nf} frames of 3840x2160 (N={N}), whole frame, {wall:.1f} s wall, "
                          f"single-threaded oracle"}
@@ -511,7 +535,7 @@ def run_band(args, rank, world, local):
             exch = "NCCL send/recv of the halo rows (baseline)"
         line = {
             "metric": "frames/s", "value": fps, "unit": "frames/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "steps": args.steps, "warmup": warm, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth/ C5bring recipe, generated on device)",
             "config": {"workload": args.config, "desc": wl["desc"], "W": W, "H": H, "N": N, "bands": G,
@@ -557,6 +581,9 @@ def main():
                     help="C5b: row bands (default: one per rank; on one process, G bands on this GPU)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="C5b under torchrun: fused peer stores + sync kernel, or NCCL send/recv baseline")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="C5b: process-group backend (gloo + --same-device: functional test on one GPU)")
+    ap.add_argument("--same-device", action="store_true", help="C5b: every rank on cuda:0 (testing only)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -149,7 +149,10 @@ class BandGroup:
     def step(self, frames, homographies, masks):
         """frames / masks: whole-frame [1][H][pitch] CUDA uint8 tensors, or per-band lists."""
         views = self.band_views(frames, masks)
-        if self.streams is None:
+        if len(self.ctxs) == 1:
+            self.ctxs[0].step(views[0][0], homographies, views[0][1],
+                              stream=self.streams[0] if self.streams else None)
+        elif self.streams is None:
             for c, (f, m) in zip(self.ctxs, views):
                 c.step(f, homographies, m)
             for c in self.ctxs:
@@ -164,6 +167,10 @@ class BandGroup:
     def step_n(self, T: int, frames, homographies, masks):
         """Per-band lists of [T][S][rows*N][pitch] tensors: one captured graph per band
         (step + sync per frame), each on its own stream."""
+        if len(self.ctxs) == 1:
+            self.ctxs[0].step_n(T, frames[0], homographies, masks[0],
+                                stream=self.streams[0] if self.streams else None)
+            return
         if self.streams is None:
             raise ValueError("step_n over bands needs one CUDA stream per band")
         for c, f, m, st in zip(self.ctxs, frames, masks, self.streams):
@@ -232,6 +239,15 @@ class BandRank:
             nxt = self.ctx.get_buffers().parity      # the buffer the step just wrote
             halo_exchange(state_view(self.ctx, nxt, self.device), self.band, self.halo, self.rank, self.world,
                           group=self.group)
+
+    def step_n(self, T: int, frames_band, homographies, masks_band, stream=None):
+        """T frames [T][S][rows*N][pitch].  peer: one CUDA graph (step + sync per frame);
+        nccl: T host-driven steps, each followed by the NCCL exchange."""
+        if self.exchange == "peer" or self.world == 1:
+            self.ctx.step_n(T, frames_band, homographies, masks_band, stream=stream)
+        else:
+            for t in range(T):
+                self.step(frames_band[t], homographies[t], masks_band[t], stream=stream)
 
     def close(self):
         self.ctx.close()
