@@ -569,7 +569,10 @@ int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double
     for (int i = 0; i < kPipeStreams; ++i)
         if ((e = cudaStreamWaitEvent(c->pipe[i], c->ev_start, 0)) != cudaSuccess) return cuda_fail(c, e, "cudaStreamWaitEvent");
     // chunks of streams: H2D(k) || kernel(k-1) || D2H(k-2) across the pipe streams
-    const int nchunks = c->S < 8 ? c->S : 8;
+    const char* cenv = getenv("DMSGM_HOST_CHUNKS");
+    int nchunks = cenv ? atoi(cenv) : 8;
+    if (nchunks < 1) nchunks = 1;
+    if (nchunks > c->S) nchunks = c->S;
     const int per = (c->S + nchunks - 1) / nchunks;
     const int parity = c->cur;
     for (int s0 = 0, k = 0; s0 < c->S; s0 += per, ++k) {
