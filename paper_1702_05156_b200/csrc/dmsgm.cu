@@ -60,7 +60,7 @@ struct dmsgm_ctx {
     int staged_occ;    // register-capped occupancy variant (3 or 4 CTAs/SM)
     int staged_ftma;   // 1: frames staged by TMA (2-stage ring); 0: 3-stage window ring + register prefetch
     int pdl;           // programmatic dependent launch of consecutive steps (DMSGM_PDL=0 disables)
-    CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (chunk-SoA, 4-D)
+    CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (4-D: 96-B chunks of 4 records)
     // row band; whole frame: row0 = 0, rows = Hb, halo = 0, band = 0
     int band, row0, rows, halo;
     int Hp;                      // pixel rows of the frames / masks passed to a step (rows * N)
@@ -230,10 +230,10 @@ KParams kparams(const dmsgm_params& p) {
 
 size_t plane_elems(const dmsgm_ctx* c) { return (size_t)c->Wb * (size_t)c->Hb; }
 int tiles_x_of(const dmsgm_ctx* c) { return (c->Wb + kTile - 1) / kTile; }
-// floats of one stream's state in the internal AoSoA layout [Hb][tiles_x][6][32]
+// floats of one stream's state in the internal layout [Hb][4*tiles_x][6] (24-byte block records)
 size_t stream_floats(const dmsgm_ctx* c) { return (size_t)c->Hb * tiles_x_of(c) * kTileFloats; }
 
-// public [6][Hb][Wb] <-> internal [Hb][tiles_x][6][32] (host side, not on the hot path)
+// public [6][Hb][Wb] <-> internal [Hb][4*tiles_x][6] (host side, not on the hot path)
 void to_public(const dmsgm_ctx* c, const float* in, float* out) {
     const size_t pe = plane_elems(c);
     const int tx = tiles_x_of(c);
@@ -241,7 +241,7 @@ void to_public(const dmsgm_ctx* c, const float* in, float* out) {
         for (int by = 0; by < c->Hb; ++by)
             for (int bx = 0; bx < c->Wb; ++bx)
                 out[p * pe + (size_t)by * c->Wb + bx] =
-                    in[((size_t)by * tx + bx / kTile) * kTileFloats + p * kTile + bx % kTile];
+                    in[(size_t)by * tx * kTileFloats + (size_t)bx * kPlanes + p];
 }
 void to_internal(const dmsgm_ctx* c, const float* in, float* out) {
     const size_t pe = plane_elems(c);
@@ -250,7 +250,7 @@ void to_internal(const dmsgm_ctx* c, const float* in, float* out) {
     for (int p = 0; p < 6; ++p)
         for (int by = 0; by < c->Hb; ++by)
             for (int bx = 0; bx < c->Wb; ++bx)
-                out[((size_t)by * tx + bx / kTile) * kTileFloats + p * kTile + bx % kTile] =
+                out[(size_t)by * tx * kTileFloats + (size_t)bx * kPlanes + p] =
                     in[p * pe + (size_t)by * c->Wb + bx];
 }
 
