@@ -54,7 +54,7 @@ typedef struct {
     float theta_s;            /* match gate of Eqs. 8-9; paper gives no value, 4 (R15) */
     float theta_d;            /* classification gate THETA_D of App. E P:657 (R14); 4 (R15)          */
     float var_init;           /* variance of a reset / new model, 255 (App. E)          */
-    float age_cap;            /* age cap, 30 (App. E AGE_THRESH P:616)                         */
+    float age_cap;            /* age cap, 30 (App. E AGE_THRESH P:616); must be in [1, 2^24]    */
     float var_floor_match;    /* variance floor in the match test, 0.1 (App. E)         */
     float var_floor_classify; /* variance floor in classification, 0.25 (App. E)               */
     float decay_lambda;       /* age-decay rate lambda (R7); 0 disables the decay bitwise             */

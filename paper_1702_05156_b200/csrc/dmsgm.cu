@@ -207,7 +207,7 @@ struct DeviceGuard {
 bool params_ok(const dmsgm_params* p, char* why, size_t n) {
     if (!p) { snprintf(why, n, "params is NULL"); return false; }
     if (!(p->theta_s > 0.f) || !(p->theta_d > 0.f)) { snprintf(why, n, "theta_s, theta_d must be > 0"); return false; }
-    if (!(p->age_cap >= 1.f) || !isfinite(p->age_cap)) { snprintf(why, n, "age_cap must be >= 1"); return false; }
+    if (!(p->age_cap >= 1.f) || !(p->age_cap <= 16777216.f)) { snprintf(why, n, "age_cap must be in [1, 2^24]"); return false; }
     if (!(p->var_init >= 0.f) || !isfinite(p->var_init)) { snprintf(why, n, "var_init must be >= 0"); return false; }
     if (!(p->var_floor_match > 0.f) || !(p->var_floor_classify > 0.f)) { snprintf(why, n, "variance floors must be > 0"); return false; }
     if (!(p->decay_lambda >= 0.f) || !(p->decay_var_thresh >= 0.f)) { snprintf(why, n, "decay params must be >= 0"); return false; }

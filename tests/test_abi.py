@@ -54,6 +54,9 @@ def test_version_and_argument_errors(built):
     bad = dm.Params(theta_s=0.0).to_c()
     assert lib.dmsgm_create(64, 48, 4, ctypes.byref(bad), 0, ctypes.byref(h)) == dm.DMSGM_EINVAL
     assert lib.dmsgm_create(64, 48, 4, None, 0, ctypes.byref(h)) == dm.DMSGM_EINVAL
+    big = dm.Params(age_cap=2.0 ** 25).to_c()        # the kernel's 1/(age+1) needs age_cap <= 2^24
+    assert lib.dmsgm_create(64, 48, 4, ctypes.byref(big), 0, ctypes.byref(h)) == dm.DMSGM_EINVAL
+    assert b"age_cap" in lib.dmsgm_last_error(None)
     assert lib.dmsgm_step(None, None, 64, None, None, 64, None) == dm.DMSGM_EINVAL
 
 
