@@ -23,6 +23,7 @@ using namespace dmsgm;
 namespace {
 
 constexpr int kPipeStreams = 3;
+constexpr int kCounterSlots = 64;   // slot 0: dmsgm_step / dmsgm_step_n; 1..: concurrent step_host chunks
 constexpr int kRowsPerCta = 4;
 
 struct GraphSlot {
@@ -58,7 +59,7 @@ struct dmsgm_ctx {
     int staged;        // 1: persistent TMA-staged kernel (N = 4, N = 8)
     int staged_ctas;   // resident CTAs of the staged kernel on this device
     int staged_occ;    // register-capped occupancy variant (3 or 4 CTAs/SM)
-    int staged_ftma;   // 1: frames staged by TMA (2-stage ring); 0: 3-stage window ring + register prefetch
+    unsigned* item_ctr;   // [kCounterSlots] dynamic item counters of the staged kernel (0 between launches)
     int pdl;           // programmatic dependent launch of consecutive steps (DMSGM_PDL=0 disables)
     CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (4-D: 96-B chunks of 4 records)
     // row band; whole frame: row0 = 0, rows = Hb, halo = 0, band = 0
@@ -119,14 +120,15 @@ bool encode_state_map(const dmsgm_ctx* c, float* base, int xc, int wrows, CUtens
 }  // namespace
 
 // Persistent TMA-staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
-template <int N, int BPT, int MINB, bool RULES, bool FTMA, bool BAND = false>
+template <int N, int BPT, int MINB, bool RULES, bool BAND = false>
 cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames, size_t fpitch, int s0,
-                          int count, int parity, cudaStream_t stream) {
+                          int count, int parity, int slot, cudaStream_t stream) {
     StagedArgs sa;
     sa.tiles_xc = (c->Wb + Staged<N, BPT>::TWB - 1) / Staged<N, BPT>::TWB;
     sa.tiles_y = (c->rows + kCtaY - 1) / kCtaY;
     sa.items = count * sa.tiles_xc * sa.tiles_y;
     sa.s0 = s0;
+    sa.ctr = c->item_ctr + slot;
     CUtensorMap fmap;
     if (!encode_frame_map(c, frames, fpitch, count, N * kCtaY, &fmap)) return cudaErrorInvalidValue;
     const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
@@ -135,42 +137,42 @@ cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(kCtaX, kCtaY + 1, 1);
-    cfg.dynamicSmemBytes = Staged<N, BPT, FTMA>::SMEM_BYTES;
+    cfg.dynamicSmemBytes = Staged<N, BPT>::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, dmsgm_step_staged<N, BPT, MINB, RULES, FTMA, BAND>, a, sa, fmap,
+    return cudaLaunchKernelEx(&cfg, dmsgm_step_staged<N, BPT, MINB, RULES, BAND>, a, sa, fmap,
                               c->state_map[parity]);
 }
 
-template <int N, int BPT, int MINB, bool FTMA>
+template <int N, int BPT, int MINB>
 cudaError_t setup_staged(dmsgm_ctx* c) {
-    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, FTMA, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT>::SMEM_BYTES);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, FTMA, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
-    if constexpr (MINB == 3 && FTMA) {   // the band-mode variants (default configuration only)
+        e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT>::SMEM_BYTES);
+    if constexpr (MINB == 3) {   // the band-mode variants (default configuration only)
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, FTMA, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
+            e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT>::SMEM_BYTES);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, FTMA, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT, FTMA>::SMEM_BYTES);
+            e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT>::SMEM_BYTES);
     }
     if (e != cudaSuccess) return e;
     int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB, false, FTMA, false>,
-                                                      kStagedThreads, Staged<N, BPT, FTMA>::SMEM_BYTES);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmsgm_step_staged<N, BPT, MINB, false, false>,
+                                                      kStagedThreads, Staged<N, BPT>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     if (e != cudaSuccess) return e;
     c->staged_ctas = (per_sm > 0 ? per_sm : 1) * sms;
     for (int i = 0; i < 2; ++i)
-        if (!encode_state_map(c, c->state[i], Staged<N, BPT, FTMA>::XC, Staged<N, BPT, FTMA>::WROWS, &c->state_map[i]))
+        if (!encode_state_map(c, c->state[i], Staged<N, BPT>::XC, Staged<N, BPT>::WROWS, &c->state_map[i]))
             return cudaErrorInvalidValue;
     return cudaSuccess;
 }
@@ -272,7 +274,7 @@ void launch_kernel(const StepArgs& a, dim3 grid, dim3 block, cudaStream_t stream
 // Enqueue one kernel for streams [s0, s0+count) of the batch.
 cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, const double* H,
                         uint8_t* masks, size_t mpitch, int s0, int count, int parity,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, int slot = 0) {
     StepArgs a;
     a.frames = frames;
     a.fstride = (long long)c->Hp * (long long)fpitch;
@@ -311,25 +313,19 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
         const bool rules = c->p.update_rule != 0 || c->p.classify_rule != 0;
         if (c->band) {   // band mode: halo check + neighbour stores compiled in
             if (c->N == 4)
-                return rules ? launch_staged<4, 2, 3, true, true, true>(c, a, frames, fpitch, s0, count, parity, stream)
-                             : launch_staged<4, 2, 3, false, true, true>(c, a, frames, fpitch, s0, count, parity, stream);
-            return rules ? launch_staged<8, 1, 3, true, true, true>(c, a, frames, fpitch, s0, count, parity, stream)
-                         : launch_staged<8, 1, 3, false, true, true>(c, a, frames, fpitch, s0, count, parity, stream);
+                return rules ? launch_staged<4, 2, 3, true, true>(c, a, frames, fpitch, s0, count, parity, slot, stream)
+                             : launch_staged<4, 2, 3, false, true>(c, a, frames, fpitch, s0, count, parity, slot, stream);
+            return rules ? launch_staged<8, 1, 3, true, true>(c, a, frames, fpitch, s0, count, parity, slot, stream)
+                         : launch_staged<8, 1, 3, false, true>(c, a, frames, fpitch, s0, count, parity, slot, stream);
         }
-#define DMSGM_STAGED(NN, BB, OO, FT)                                                                        \
-    return rules ? launch_staged<NN, BB, OO, true, FT>(c, a, frames, fpitch, s0, count, parity, stream)    \
-                 : launch_staged<NN, BB, OO, false, FT>(c, a, frames, fpitch, s0, count, parity, stream)
-#define DMSGM_STAGED_OCC(NN, BB, FT)       \
-    if (c->staged_occ == 3) DMSGM_STAGED(NN, BB, 3, FT); \
-    DMSGM_STAGED(NN, BB, 4, FT)
-        if (c->N == 4) {
-            if (c->staged_ftma) { DMSGM_STAGED_OCC(4, 2, true); }
-            DMSGM_STAGED_OCC(4, 2, false);
-        }
-        if (c->N == 8) {
-            if (c->staged_ftma) { DMSGM_STAGED_OCC(8, 1, true); }
-            DMSGM_STAGED_OCC(8, 1, false);
-        }
+#define DMSGM_STAGED(NN, BB, OO)                                                                            \
+    return rules ? launch_staged<NN, BB, OO, true>(c, a, frames, fpitch, s0, count, parity, slot, stream)    \
+                 : launch_staged<NN, BB, OO, false>(c, a, frames, fpitch, s0, count, parity, slot, stream)
+#define DMSGM_STAGED_OCC(NN, BB)                      \
+    if (c->staged_occ == 3) { DMSGM_STAGED(NN, BB, 3); } \
+    DMSGM_STAGED(NN, BB, 4)
+        if (c->N == 4) { DMSGM_STAGED_OCC(4, 2); }
+        if (c->N == 8) { DMSGM_STAGED_OCC(8, 1); }
 #undef DMSGM_STAGED_OCC
 #undef DMSGM_STAGED
     }
@@ -439,11 +435,7 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
             c->staged_occ = (oenv && atoi(oenv) == 4) ? 4 : 3;
             const char* penv = getenv("DMSGM_PDL");
             c->pdl = !(penv && atoi(penv) == 0);
-            const char* fenv = getenv("DMSGM_STAGED_FRAMES");  // "tma" (default) or "regs"
-            c->staged_ftma = !(fenv && strcmp(fenv, "regs") == 0);
-#define DMSGM_SETUP(NN, BB)                                                                   \
-    (c->staged_ftma ? (c->staged_occ == 3 ? setup_staged<NN, BB, 3, true>(c) : setup_staged<NN, BB, 4, true>(c)) \
-                    : (c->staged_occ == 3 ? setup_staged<NN, BB, 3, false>(c) : setup_staged<NN, BB, 4, false>(c)))
+#define DMSGM_SETUP(NN, BB) (c->staged_occ == 3 ? setup_staged<NN, BB, 3>(c) : setup_staged<NN, BB, 4>(c))
             e = block == 4 ? DMSGM_SETUP(4, 2) : DMSGM_SETUP(8, 1);
 #undef DMSGM_SETUP
             if (e != cudaSuccess) {
@@ -453,7 +445,9 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
             c->staged = 1;
         }
     }
-    if ((e = cudaMalloc(&c->flags, 3 * sizeof(unsigned))) != cudaSuccess ||
+    if ((e = cudaMalloc(&c->item_ctr, kCounterSlots * sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMemset(c->item_ctr, 0, kCounterSlots * sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMalloc(&c->flags, 3 * sizeof(unsigned))) != cudaSuccess ||
         (e = cudaHostAlloc(&c->status_host, sizeof(unsigned), cudaHostAllocMapped)) != cudaSuccess ||
         (e = cudaHostGetDevicePointer(&c->status_dev, c->status_host, 0)) != cudaSuccess) {
         dmsgm_destroy(c);
@@ -586,7 +580,9 @@ int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double
         if ((e = cudaMemcpyAsync(c->st_H + (size_t)s0 * 9, hH + (size_t)s0 * 9, (size_t)cnt * 9 * sizeof(double),
                                  cudaMemcpyHostToDevice, st)) != cudaSuccess)
             return cuda_fail(c, e, "H2D homographies");
-        if ((e = launch_step(c, df, dpitch, c->st_H + (size_t)s0 * 9, dm, dpitch, s0, cnt, parity, st)) != cudaSuccess)
+        // chunks run concurrently on the pipe streams: each its own item-counter slot
+        if ((e = launch_step(c, df, dpitch, c->st_H + (size_t)s0 * 9, dm, dpitch, s0, cnt, parity, st,
+                             1 + k % (kCounterSlots - 1))) != cudaSuccess)
             return cuda_fail(c, e, "dmsgm_step_host launch");
         if ((e = cudaMemcpy2DAsync(hm + (size_t)s0 * c->Hp * mpitch, mpitch, dm, dpitch, c->W, (size_t)cnt * c->Hp,
                                    cudaMemcpyDeviceToHost, st)) != cudaSuccess)
@@ -681,7 +677,7 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
                                        24.0 * (double)c->Wb * c->halo * nb;
     if (c->staged)
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d,%s> (TMA, persistent)", c->N,
-                 c->N == 4 ? 2 : 1, c->staged_occ, c->staged_ftma ? "frames:tma" : "frames:regs");
+                 c->N == 4 ? 2 : 1, c->staged_occ, "frames:tma");
     else
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_kernel<%d,%d>", c->N, bpt_of(c));
     if (c->staged && c->band)
@@ -726,12 +722,11 @@ int dmsgm_set_band(dmsgm_ctx* c, int row0, int rows, int halo) {
     detach(c, 0);
     detach(c, 1);
     const bool whole = row0 == 0 && rows == c->Hb && halo == 0;
-    if (!whole && c->staged && (c->staged_occ != 3 || !c->staged_ftma)) {
+    if (!whole && c->staged && c->staged_occ != 3) {
         // the band kernels exist in the default configuration only
-        e = c->N == 4 ? setup_staged<4, 2, 3, true>(c) : setup_staged<8, 1, 3, true>(c);
+        e = c->N == 4 ? setup_staged<4, 2, 3>(c) : setup_staged<8, 1, 3>(c);
         if (e != cudaSuccess) return cuda_fail(c, e, "band kernel setup");
         c->staged_occ = 3;
-        c->staged_ftma = 1;
     }
     c->band = whole ? 0 : 1;
     c->row0 = row0;
@@ -905,6 +900,7 @@ void dmsgm_destroy(dmsgm_ctx* c) {
         for (int k = 0; k < 3; ++k)
             if (c->ipc_open[side][k]) cudaIpcCloseMemHandle(c->ipc_open[side][k]);
     if (c->flags) cudaFree(c->flags);
+    if (c->item_ctr) cudaFree(c->item_ctr);
     if (c->status_host) cudaFreeHost(c->status_host);
     for (int i = 0; i < 2; ++i) {
         if (c->state[i]) cudaFree(c->state[i]);
