@@ -41,6 +41,7 @@ WORKLOADS = {
     "C4": dict(ring="C4ring", desc="1920x1080 u8, 4x4 blocks, 32 streams/GPU"),
     "C5": dict(ring="C5ring", desc="3840x2160 u8, 8x8 blocks, 64 streams/GPU"),
     "C5b": dict(ring="C5bring", desc="3840x2160 u8, 8x8 blocks, ONE stream split into row bands"),
+    "C4p": dict(ring="C4pring", desc="1920x1080 u8, per-pixel models (block 1, NEXT-1), 4 streams/GPU"),
 }
 
 
@@ -185,7 +186,7 @@ def run_reference(args, rank, world):
     ns = max(1, min(cfg.S, cores))
     seq = synth.generate(cfg, T=2, streams=range(min(ns, 4)))
     frames, Hs = seq.frames, seq.homographies
-    est_frame_s = 0.025 * (cfg.W * cfg.H) / (1920 * 1080)
+    est_frame_s = 0.025 * (cfg.W * cfg.H) / (1920 * 1080) * (0.4 + 9.6 / cfg.N ** 2)
     budget = 150.0
     while ns > 1 and (args.steps + args.warmup) * est_frame_s * math.ceil(ns / cores) > budget:
         ns = max(1, ns // 2)
@@ -326,7 +327,7 @@ def run_dmsgm(args, rank, world, local):
         ns = min(S, cores)
         fh = frames[:2, :ns].cpu().numpy()
         target_s = args.cpu_seconds
-        per_frame = 0.021 * (W * H) / (1920 * 1080)
+        per_frame = 0.021 * (W * H) / (1920 * 1080) * (0.4 + 9.6 / N ** 2)   # oracle s/frame (per-block work ~ 1/N^2)
         nf = max(2, int(target_s / per_frame / ns * min(cores, ns)))
         cfps, used, wall = oracle_throughput(cfg, fh, Hs[:2, :ns], ns, nf, cores)
         cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle",
@@ -515,7 +516,7 @@ def run_band(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         seq = synth.generate(cfg, T=2)
-        per_frame = 0.021 * (W * H) / (1920 * 1080)
+        per_frame = 0.021 * (W * H) / (1920 * 1080) * (0.4 + 9.6 / N ** 2)   # oracle s/frame (per-block work ~ 1/N^2)
         nf = max(2, int(args.cpu_seconds / per_frame))
         cfps, used, wall = oracle_throughput(cfg, seq.frames, seq.homographies, 1, nf, 1)
         cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle",

@@ -89,14 +89,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // 4-D view of a state buffer: {24 floats of a chunk, chunks per row, block rows, streams}.
-// 3-D view of a frame batch: {width bytes, rows, streams}; box 256 B x rows x 1.
-bool encode_frame_map(const dmsgm_ctx* c, const uint8_t* base, size_t pitch, int count, int box_rows,
-                      CUtensorMap* out) {
+// 3-D view of a frame batch: {width bytes, rows, streams}; box (32 x N x BPT) B x rows x 1.
+bool encode_frame_map(const dmsgm_ctx* c, const uint8_t* base, size_t pitch, int count, int box_cols,
+                      int box_rows, CUtensorMap* out) {
     auto enc = tensor_map_encoder();
     if (!enc) return false;
     cuuint64_t dims[3] = {(cuuint64_t)c->W, (cuuint64_t)c->Hp, (cuuint64_t)count};
     cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * c->Hp};
-    cuuint32_t box[3] = {256, (cuuint32_t)box_rows, 1};
+    cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -130,7 +130,8 @@ cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames
     sa.s0 = s0;
     sa.ctr = c->item_ctr + slot;
     CUtensorMap fmap;
-    if (!encode_frame_map(c, frames, fpitch, count, N * kCtaY, &fmap)) return cudaErrorInvalidValue;
+    if (!encode_frame_map(c, frames, fpitch, count, Staged<N, BPT>::FROW_BYTES, N * kCtaY, &fmap))
+        return cudaErrorInvalidValue;
     const int grid = sa.items < c->staged_ctas ? sa.items : c->staged_ctas;
     // programmatic dependent launch: may begin while the previous step drains; the kernel
     // itself waits (griddepcontrol.wait) before touching the state the previous step wrote
@@ -311,19 +312,24 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
         // RULES = the App. E compatibility switches (R27/R28) are on: runtime-switched code;
         // otherwise the default rules are compiled in without branches.
         const bool rules = c->p.update_rule != 0 || c->p.classify_rule != 0;
+#define DMSGM_BAND(NN, BB)                                                                                    \
+    return rules ? launch_staged<NN, BB, 3, true, true>(c, a, frames, fpitch, s0, count, parity, slot, stream) \
+                 : launch_staged<NN, BB, 3, false, true>(c, a, frames, fpitch, s0, count, parity, slot, stream)
         if (c->band) {   // band mode: halo check + neighbour stores compiled in
-            if (c->N == 4)
-                return rules ? launch_staged<4, 2, 3, true, true>(c, a, frames, fpitch, s0, count, parity, slot, stream)
-                             : launch_staged<4, 2, 3, false, true>(c, a, frames, fpitch, s0, count, parity, slot, stream);
-            return rules ? launch_staged<8, 1, 3, true, true>(c, a, frames, fpitch, s0, count, parity, slot, stream)
-                         : launch_staged<8, 1, 3, false, true>(c, a, frames, fpitch, s0, count, parity, slot, stream);
+            if (c->N == 1) { DMSGM_BAND(1, 2); }
+            if (c->N == 2) { DMSGM_BAND(2, 2); }
+            if (c->N == 4) { DMSGM_BAND(4, 2); }
+            DMSGM_BAND(8, 1);
         }
+#undef DMSGM_BAND
 #define DMSGM_STAGED(NN, BB, OO)                                                                            \
     return rules ? launch_staged<NN, BB, OO, true>(c, a, frames, fpitch, s0, count, parity, slot, stream)    \
                  : launch_staged<NN, BB, OO, false>(c, a, frames, fpitch, s0, count, parity, slot, stream)
 #define DMSGM_STAGED_OCC(NN, BB)                      \
     if (c->staged_occ == 3) { DMSGM_STAGED(NN, BB, 3); } \
     DMSGM_STAGED(NN, BB, 4)
+        if (c->N == 1) { DMSGM_STAGED(1, 2, 3); }
+        if (c->N == 2) { DMSGM_STAGED(2, 2, 3); }
         if (c->N == 4) { DMSGM_STAGED_OCC(4, 2); }
         if (c->N == 8) { DMSGM_STAGED_OCC(8, 1); }
 #undef DMSGM_STAGED_OCC
@@ -430,13 +436,16 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
         const char* kenv = getenv("DMSGM_KERNEL");           // "generic" forces the register-path kernel
         const bool want = !(kenv && strcmp(kenv, "generic") == 0);
         c->staged = 0;
-        if (want && (block == 4 || block == 8)) {
+        if (want && block != 16) {   // N = 16: a 512-byte frame row exceeds the TMA box limit
             const char* oenv = getenv("DMSGM_STAGED_OCC");   // 3 or 4 resident CTAs per SM (register cap)
             c->staged_occ = (oenv && atoi(oenv) == 4) ? 4 : 3;
             const char* penv = getenv("DMSGM_PDL");
             c->pdl = !(penv && atoi(penv) == 0);
 #define DMSGM_SETUP(NN, BB) (c->staged_occ == 3 ? setup_staged<NN, BB, 3>(c) : setup_staged<NN, BB, 4>(c))
-            e = block == 4 ? DMSGM_SETUP(4, 2) : DMSGM_SETUP(8, 1);
+            if (block < 4) c->staged_occ = 3;   // (the 4-CTA variants exist for N = 4 and 8 only)
+            e = block == 1 ? setup_staged<1, 2, 3>(c)
+              : block == 2 ? setup_staged<2, 2, 3>(c)
+              : block == 4 ? DMSGM_SETUP(4, 2) : DMSGM_SETUP(8, 1);
 #undef DMSGM_SETUP
             if (e != cudaSuccess) {
                 dmsgm_destroy(c);
@@ -676,13 +685,13 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     out->algorithmic_bytes_per_frame = 2.0 * c->W * c->Hp + 2.0 * 24.0 * (double)c->Wb * c->rows +
                                        24.0 * (double)c->Wb * c->halo * nb;
     if (c->staged)
-        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d,%s> (TMA, persistent)", c->N,
-                 c->N == 4 ? 2 : 1, c->staged_occ, "frames:tma");
+        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d> (TMA, persistent)", c->N,
+                 c->N == 8 ? 1 : 2, c->staged_occ);
     else
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_kernel<%d,%d>", c->N, bpt_of(c));
     if (c->staged && c->band)
-        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,3,frames:tma,band> (TMA, persistent)",
-                 c->N, c->N == 4 ? 2 : 1);
+        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,3,band> (TMA, persistent)",
+                 c->N, c->N == 8 ? 1 : 2);
     return DMSGM_OK;
 }
 
@@ -724,7 +733,7 @@ int dmsgm_set_band(dmsgm_ctx* c, int row0, int rows, int halo) {
     const bool whole = row0 == 0 && rows == c->Hb && halo == 0;
     if (!whole && c->staged && c->staged_occ != 3) {
         // the band kernels exist in the default configuration only
-        e = c->N == 4 ? setup_staged<4, 2, 3>(c) : setup_staged<8, 1, 3>(c);
+        e = c->N == 4 ? setup_staged<4, 2, 3>(c) : setup_staged<8, 1, 3>(c);   // (N < 4 is always 3)
         if (e != cudaSuccess) return cuda_fail(c, e, "band kernel setup");
         c->staged_occ = 3;
     }

@@ -68,6 +68,9 @@ CONFIGS = {
                         rot_deg=0.05, zoom=0.0005, n_objects=(4, 8), period=8),
     "C5ring": SeqConfig("C5ring", 3840, 2160, 8, 64, 8, 5000, 2.0, "ring", pan=(4.0, 4.0),
                         rot_deg=0.05, zoom=0.0005, n_objects=(4, 8), period=8),
+    # C4p: the paper's own per-pixel DSGM (block = 1) at 1080p, 4 streams
+    "C4pring": SeqConfig("C4pring", 1920, 1080, 1, 4, 8, 4100, 2.0, "ring", pan=(2.0, 2.0),
+                         rot_deg=0.05, zoom=0.0005, n_objects=(4, 8), period=8),
     # C5b: ONE 4K stream split into row bands over the GPUs; motion
     # small enough (pan <= 2 px, rotation <= 0.02 deg per frame) for a one-block-row halo
     "C5b": SeqConfig("C5b", 3840, 2160, 8, 1, 100, 5100, 2.0, "random", pan=(2.0, 2.0),
