@@ -20,6 +20,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dmsgm_oracle.c")
+_SRC2 = os.path.join(_HERE, "prefilter_oracle.c")
 _HDR = os.path.join(_HERE, "dmsgm_oracle.h")
 LIB_PATH = os.path.join(_HERE, "libdmsgm_oracle.so")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
@@ -31,10 +32,10 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile the oracle into oracle/libdmsgm_oracle.so (gcc, no FMA contraction)."""
-    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC2), os.path.getmtime(_HDR))
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
         tmp = LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC2, "-lm"])
         os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
@@ -69,6 +70,8 @@ def _load():
             lib.dmsgm_oracle_mix_weights.argtypes = [i32, i32, i32, P, i32, i32, P, P, P, P]
             lib.dmsgm_oracle_decay_exp.argtypes = [ctypes.c_float]
             lib.dmsgm_oracle_decay_exp.restype = ctypes.c_float
+            lib.dmsgm_oracle_gauss_taps.argtypes = [i32, ctypes.c_float, P]
+            lib.dmsgm_oracle_prefilter.argtypes = [i32, i32, P, sz, P, sz, i32, ctypes.c_float, i32]
             _lib = lib
     return _lib
 
@@ -167,6 +170,35 @@ class Oracle:
 def decay_exp(x: float) -> float:
     """exp(-x) as the oracle evaluates it (reading R18)."""
     return float(_load().dmsgm_oracle_decay_exp(x))
+
+
+def gauss_taps(size: int, sigma: float) -> np.ndarray:
+    """The normalised fp32 Gaussian taps of reading R30."""
+    t = np.zeros(size, np.float32)
+    if _load().dmsgm_oracle_gauss_taps(size, sigma, _ptr(t)) != 0:
+        raise ValueError("bad taps arguments")
+    return t
+
+
+def prefilter(frame: np.ndarray, gauss_size: int = 5, gauss_sigma: float = 1.0, median_radius: int = 1) -> np.ndarray:
+    """§2.1 preprocessing of one u8 frame [H][W] (readings R30-R34): separable Gaussian, then median."""
+    f = np.ascontiguousarray(frame, np.uint8)
+    H, W = f.shape
+    out = np.empty_like(f)
+    if _load().dmsgm_oracle_prefilter(W, H, _ptr(f), W, _ptr(out), W, gauss_size, gauss_sigma, median_radius) != 0:
+        raise ValueError("bad prefilter arguments")
+    return out
+
+
+def prefilter_frames(frames: np.ndarray, gauss_size: int = 5, gauss_sigma: float = 1.0,
+                     median_radius: int = 1) -> np.ndarray:
+    """prefilter() over [..., H, W]."""
+    out = np.empty_like(frames)
+    flat_in = frames.reshape(-1, *frames.shape[-2:])
+    flat_out = out.reshape(-1, *frames.shape[-2:])
+    for i in range(flat_in.shape[0]):
+        flat_out[i] = prefilter(flat_in[i], gauss_size, gauss_sigma, median_radius)
+    return out
 
 
 def mix_weights(width: int, height: int, block: int, h, bi: int, bj: int, with_clipped: bool = False):

@@ -73,6 +73,14 @@ int dmsgm_oracle_mix_weights(int width, int height, int block, const double* h, 
 /* The decay factor exp(-x) of reading R18 (exposed for its pin). */
 float dmsgm_oracle_decay_exp(float x);
 
+/* Frame preprocessing of §2.1 / §3.3.1 / App. A-B (prefilter_oracle.c, readings R30-R34):
+ * the normalised Gaussian taps (size odd <= 15, sigma > 0), and the separable Gaussian
+ * (gauss_size 1 = off) followed by the clamped median of radius median_radius
+ * (0 = off, <= 4) of one u8 frame. */
+int dmsgm_oracle_gauss_taps(int size, float sigma, float* taps);
+int dmsgm_oracle_prefilter(int width, int height, const uint8_t* in, size_t in_pitch, uint8_t* out,
+                           size_t out_pitch, int gauss_size, float gauss_sigma, int median_radius);
+
 #ifdef __cplusplus
 }
 #endif
