@@ -140,7 +140,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (test infrastructure; the only other place bench.py runs oracle/)
 # ---------------------------------------------------------------------------
-def oracle_throughput(cfg, frames_host, Hs, n_streams, n_frames, threads):
+def oracle_throughput(cfg, frames_host, Hs, n_streams, n_frames, threads, prefilter=None):
     """Oracle frames/s on `n_streams` streams x `n_frames` frames, one thread per stream
     (ctypes releases the GIL; the oracle itself is single-threaded).  Returns (fps, cores, wall)."""
     import oracle
@@ -152,7 +152,10 @@ def oracle_throughput(cfg, frames_host, Hs, n_streams, n_frames, threads):
 
     def run_frame(t):
         def one(s):
-            o.step_stream(s, frames_host[t % R, s % frames_host.shape[1]], Hs[t % R, s % Hs.shape[1]], masks[s])
+            fr = frames_host[t % R, s % frames_host.shape[1]]
+            if prefilter:
+                fr = oracle.prefilter(fr, *prefilter)
+            o.step_stream(s, fr, Hs[t % R, s % Hs.shape[1]], masks[s])
         with ThreadPoolExecutor(max_workers=threads) as ex:
             list(ex.map(one, range(n_streams)))
         o.commit()
@@ -257,6 +260,11 @@ def run_dmsgm(args, rank, world, local):
     masks = torch.empty_like(frames)
     params = method_params(dm, S)
     ctx = dm.Dmsgm(W, H, N, params, device=local)
+    pf = None
+    if args.prefilter:
+        gs, sg, mr = args.prefilter.split(",")
+        pf = (int(gs), float(sg), int(mr))
+        ctx.set_prefilter(*pf)                  # Gaussian + median before the step
     info = ctx.info
     stream = torch.cuda.current_stream(dev)
     bytes_per_step = S * info.algorithmic_bytes_per_frame
@@ -328,8 +336,10 @@ def run_dmsgm(args, rank, world, local):
         fh = frames[:2, :ns].cpu().numpy()
         target_s = args.cpu_seconds
         per_frame = 0.021 * (W * H) / (1920 * 1080) * (0.4 + 9.6 / N ** 2)   # oracle s/frame (per-block work ~ 1/N^2)
+        if pf:
+            per_frame += 0.15 * (W * H) / (1920 * 1080)                      # + the oracle's filters
         nf = max(2, int(target_s / per_frame / ns * min(cores, ns)))
-        cfps, used, wall = oracle_throughput(cfg, fh, Hs[:2, :ns], ns, nf, cores)
+        cfps, used, wall = oracle_throughput(cfg, fh, Hs[:2, :ns], ns, nf, cores, prefilter=pf)
         cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle",
                "sample": f"{ns} streams x {nf} frames of {wl['desc'].split(',')[0]} (N={N}), "
                          f"{wall:.1f} s wall, one single-threaded oracle step per stream per thread"}
@@ -344,7 +354,9 @@ def run_dmsgm(args, rank, world, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth/ ring recipe, generated on device)",
-            "config": {"workload": args.config, "desc": wl["desc"], "W": W, "H": H, "N": N,
+            "config": {"workload": args.config + ("+prefilter" if pf else ""), "desc": wl["desc"], "W": W, "H": H,
+                       "N": N, "prefilter": {"gauss_size": pf[0], "gauss_sigma": pf[1], "median_radius": pf[2]}
+                       if pf else None,
                        "streams_per_gpu": S, "total_streams": total_streams, "ring_frames": RING,
                        "l2": f"inputs larger than L2: {bytes_per_step / 1e6:.1f} MB algorithmic traffic per step "
                              f"(ring of {RING} distinct frames/masks per stream, {2 * RING * S * W * H / 1e9:.2f} GB)",
@@ -354,7 +366,8 @@ def run_dmsgm(args, rank, world, local):
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_step,
                          "peak_source": peak_src,
-                         "kernel": f"{kernel_name} (1 launch/step)"},
+                         "kernel": f"{kernel_name} ({info.kernels_per_step} launch(es)/step"
+                                   f"{', + dmsgm_prefilter_kernel' if pf else ''})"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": info.kernels_per_step * args.steps,
@@ -582,6 +595,8 @@ def main():
                     help="C5b: row bands (default: one per rank; on one process, G bands on this GPU)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="C5b under torchrun: fused peer stores + sync kernel, or NCCL send/recv baseline")
+    ap.add_argument("--prefilter", default="",
+                    help="GAUSS_SIZE,SIGMA,MEDIAN_RADIUS (e.g. 5,1.0,1): NEXT-2 preprocessing before every step")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="C5b: process-group backend (gloo + --same-device: functional test on one GPU)")
     ap.add_argument("--same-device", action="store_true", help="C5b: every rank on cuda:0 (testing only)")

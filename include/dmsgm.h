@@ -138,6 +138,27 @@ const char* dmsgm_last_error(const dmsgm_ctx* ctx);
 void dmsgm_destroy(dmsgm_ctx* ctx);
 
 /* ------------------------------------------------------------------------------------
+ * Frame preprocessing: PAPER.md §2.1 pre-processes
+ * the incoming frame with "a Gaussian filter and a median filter"; §3.3.1
+ * and App. A/B give the implementation.  DESIGN.md readings R30-R34: separable Gaussian
+ * of odd size gauss_size (1 = off, 3, 5, 7) and std gauss_sigma > 0 in fp32 (row pass,
+ * then column pass rounded once to u8), then the clamped 3x3 median (median_radius 1;
+ * 0 = off); image borders clamp.
+ * ------------------------------------------------------------------------------------ */
+
+/* Filter every step's frames before the step (the filtered frame replaces the frame for
+ * S4 and S8).  Allocates a filtered-frame buffer of S * height * round_up(width, 16)
+ * bytes; one extra kernel per step.  (1, *, 0) switches it off.  Not available in
+ * row-band mode (DMSGM_ESTATE).  Synchronises the device. */
+int dmsgm_set_prefilter(dmsgm_ctx* ctx, int gauss_size, float gauss_sigma, int median_radius);
+
+/* Stand-alone filter of `count` frames: in u8 [count][height][in_pitch], out u8
+ * [count][height][out_pitch] (device; width % 4 == 0, out 4-byte aligned, out_pitch % 4
+ * == 0).  Enqueued on cuda_stream; DMSGM_EINVAL for bad arguments. */
+int dmsgm_prefilter(int width, int height, int count, const uint8_t* in, size_t in_pitch, uint8_t* out,
+                    size_t out_pitch, int gauss_size, float gauss_sigma, int median_radius, void* cuda_stream);
+
+/* ------------------------------------------------------------------------------------
  * Row-band split of one large frame over several GPUs (
  * north_star: "a single very large frame may optionally be split into row bands with
  * a one-block-row halo exchanged over NVLink").  Only S1-S2 read neighbouring blocks

@@ -17,6 +17,7 @@
 
 #include "dmsgm.h"
 #include "dmsgm_kernel.cuh"
+#include "dmsgm_prefilter.cuh"
 
 using namespace dmsgm;
 
@@ -72,6 +73,12 @@ struct dmsgm_ctx {
     float* peer_state[2][2];     // [side][buffer]: neighbours' state buffers (side 0 upper, 1 lower)
     unsigned* peer_slot[2];      // neighbour's flag word that we signal
     void* ipc_open[2][3];        // IPC mappings to close at destroy
+    // preprocessing: Gaussian radius, median radius, taps,
+    // and the filtered-frame buffer the step reads ([S][Hp][pf_pitch])
+    int pf_g, pf_m;
+    float pf_taps[2 * kPfMaxG + 1];
+    uint8_t* pf_buf;
+    size_t pf_pitch;
     char err[512];
 };
 
@@ -267,6 +274,45 @@ int bpt_of(const dmsgm_ctx* c) {
     }
 }
 
+// R30: normalised Gaussian taps (fp64 exp and normalisation, rounded to fp32)
+bool gauss_taps(int size, float sigma, float* taps) {
+    if (size < 1 || size % 2 == 0 || size > 2 * kPfMaxG + 1 || !(sigma > 0.0f)) return false;
+    const int c = (size - 1) / 2;
+    double t[2 * kPfMaxG + 1], sum = 0.0;
+    for (int i = 0; i < size; ++i) {
+        const double x = (double)(i - c);
+        t[i] = exp(-(x * x) / (2.0 * (double)sigma * (double)sigma));
+        sum += t[i];
+    }
+    for (int i = 0; i < size; ++i) taps[i] = (float)(t[i] / sum);
+    return true;
+}
+
+cudaError_t launch_prefilter(int W, int H, int count, const uint8_t* in, long long in_stride, size_t in_pitch,
+                             uint8_t* out, long long out_stride, size_t out_pitch, int g, int m, const float* taps,
+                             cudaStream_t stream) {
+    PrefilterArgs a;
+    a.in = in; a.in_stride = in_stride; a.in_pitch = (int)in_pitch;
+    a.out = out; a.out_stride = out_stride; a.out_pitch = (int)out_pitch;
+    a.W = W; a.H = H; a.g = g; a.m = m;
+    for (int i = 0; i < 2 * kPfMaxG + 1; ++i) a.taps[i] = i < 2 * g + 1 ? taps[i] : 0.0f;
+    const dim3 grid((W + kPfTileX - 1) / kPfTileX, (H + kPfTileY - 1) / kPfTileY, count);
+#define DMSGM_PF(GG, MM) dmsgm_prefilter_kernel<GG, MM><<<grid, kPfThreads, 0, stream>>>(a)
+    switch (g * 2 + m) {
+        case 0: DMSGM_PF(0, 0); break;
+        case 1: DMSGM_PF(0, 1); break;
+        case 2: DMSGM_PF(1, 0); break;
+        case 3: DMSGM_PF(1, 1); break;
+        case 4: DMSGM_PF(2, 0); break;
+        case 5: DMSGM_PF(2, 1); break;
+        case 6: DMSGM_PF(3, 0); break;
+        case 7: DMSGM_PF(3, 1); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef DMSGM_PF
+    return cudaGetLastError();
+}
+
 template <int N, int BPT>
 void launch_kernel(const StepArgs& a, dim3 grid, dim3 block, cudaStream_t stream) {
     dmsgm_step_kernel<N, BPT><<<grid, block, 0, stream>>>(a);
@@ -276,6 +322,16 @@ void launch_kernel(const StepArgs& a, dim3 grid, dim3 block, cudaStream_t stream
 cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, const double* H,
                         uint8_t* masks, size_t mpitch, int s0, int count, int parity,
                         cudaStream_t stream, int slot = 0) {
+    if (c->pf_buf) {
+        // preprocessing (R34): the filtered frames replace the frames for the whole step
+        uint8_t* pf = c->pf_buf + (size_t)s0 * c->Hp * c->pf_pitch;
+        cudaError_t e = launch_prefilter(c->W, c->Hp, count, frames, (long long)c->Hp * fpitch, fpitch, pf,
+                                         (long long)c->Hp * c->pf_pitch, c->pf_pitch, c->pf_g, c->pf_m, c->pf_taps,
+                                         stream);
+        if (e != cudaSuccess) return e;
+        frames = pf;
+        fpitch = c->pf_pitch;
+    }
     StepArgs a;
     a.frames = frames;
     a.fstride = (long long)c->Hp * (long long)fpitch;
@@ -361,6 +417,7 @@ int check_images(dmsgm_ctx* c, const void* frames, size_t fpitch, const void* H,
 }
 
 bool has_peers(const dmsgm_ctx* c) { return c->peer_slot[0] || c->peer_slot[1]; }
+
 
 // Enqueue the band signal / wait kernel (one thread).
 cudaError_t launch_sync(dmsgm_ctx* c, int signal, int wait, cudaStream_t stream) {
@@ -676,7 +733,7 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     if (!c || !out) return DMSGM_EINVAL;
     out->width = c->W; out->height = c->H; out->block = c->N;
     out->blocks_x = c->Wb; out->blocks_y = c->Hb; out->num_streams = c->S;
-    out->kernels_per_step = has_peers(c) ? 2 : 1;
+    out->kernels_per_step = (has_peers(c) ? 2 : 1) + (c->pf_buf ? 1 : 0);
     out->band_row0 = c->row0; out->band_rows = c->rows; out->band_halo = c->halo;
     out->state_bytes = (size_t)c->S * stream_floats(c) * sizeof(float);
     // frame read (1 B/px) + mask write (1 B/px) + state read + write (2 x 24 B per block)
@@ -684,6 +741,8 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     const int nb = (c->peer_slot[0] ? 1 : 0) + (c->peer_slot[1] ? 1 : 0);
     out->algorithmic_bytes_per_frame = 2.0 * c->W * c->Hp + 2.0 * 24.0 * (double)c->Wb * c->rows +
                                        24.0 * (double)c->Wb * c->halo * nb;
+    // preprocessing as its own kernel: + read the frame + write the filtered frame
+    if (c->pf_buf) out->algorithmic_bytes_per_frame += 2.0 * c->W * c->Hp;
     if (c->staged)
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d> (TMA, persistent)", c->N,
                  c->N == 8 ? 1 : 2, c->staged_occ);
@@ -692,6 +751,49 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     if (c->staged && c->band)
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,3,band> (TMA, persistent)",
                  c->N, c->N == 8 ? 1 : 2);
+    return DMSGM_OK;
+}
+
+// ---- preprocessing ----
+
+int dmsgm_prefilter(int width, int height, int count, const uint8_t* in, size_t in_pitch, uint8_t* out,
+                    size_t out_pitch, int gauss_size, float gauss_sigma, int median_radius, void* stream) {
+    float taps[2 * kPfMaxG + 1];
+    if (!in || !out || width < 4 || width % 4 || height < 1 || count < 1 || in_pitch < (size_t)width ||
+        out_pitch < (size_t)width || (out_pitch & 3) || ((uintptr_t)out & 3))
+        return DMSGM_EINVAL;
+    if (median_radius < 0 || median_radius > 1 || !gauss_taps(gauss_size, gauss_sigma, taps)) return DMSGM_EINVAL;
+    cudaError_t e = launch_prefilter(width, height, count, in, (long long)height * in_pitch, in_pitch, out,
+                                     (long long)height * out_pitch, out_pitch, (gauss_size - 1) / 2, median_radius,
+                                     taps, (cudaStream_t)stream);
+    return e == cudaSuccess ? DMSGM_OK : DMSGM_ECUDA;
+}
+
+int dmsgm_set_prefilter(dmsgm_ctx* c, int gauss_size, float gauss_sigma, int median_radius) {
+    if (!c) return DMSGM_EINVAL;
+    float taps[2 * kPfMaxG + 1];
+    if (median_radius < 0 || median_radius > 1 || !gauss_taps(gauss_size, gauss_sigma, taps))
+        return fail(c, DMSGM_EINVAL, "gauss_size must be 1, 3, 5 or 7, sigma > 0, median_radius 0 or 1");
+    if (c->band) return fail(c, DMSGM_ESTATE, "preprocessing is not supported in row-band mode");
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_set_prefilter sync");
+    destroy_graphs(c);
+    const bool on = gauss_size > 1 || median_radius > 0;
+    if (c->pf_buf && !on) {
+        cudaFree(c->pf_buf);
+        c->pf_buf = nullptr;
+    }
+    if (on && !c->pf_buf) {
+        c->pf_pitch = ((size_t)c->W + 15) & ~(size_t)15;
+        if ((e = cudaMalloc(&c->pf_buf, (size_t)c->S * c->H * c->pf_pitch)) != cudaSuccess) {
+            c->pf_buf = nullptr;
+            return fail(c, DMSGM_ENOMEM, "filtered-frame buffer: %s", cudaGetErrorString(e));
+        }
+    }
+    c->pf_g = (gauss_size - 1) / 2;
+    c->pf_m = median_radius;
+    for (int i = 0; i < 2 * kPfMaxG + 1; ++i) c->pf_taps[i] = i < gauss_size ? taps[i] : 0.0f;
     return DMSGM_OK;
 }
 
@@ -723,6 +825,8 @@ int dmsgm_set_band(dmsgm_ctx* c, int row0, int rows, int halo) {
     if (row0 < 0 || rows < 1 || row0 + rows > c->Hb)
         return fail(c, DMSGM_EINVAL, "band rows [%d, %d) outside [0, %d)", row0, row0 + rows, c->Hb);
     if (halo < 0 || halo > rows) return fail(c, DMSGM_EINVAL, "halo must be in [0, rows]");
+    if (c->pf_buf && !(row0 == 0 && rows == c->Hb && halo == 0))
+        return fail(c, DMSGM_ESTATE, "preprocessing is not supported in row-band mode");
     DeviceGuard g(c->device);
     if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
     cudaError_t e = cudaDeviceSynchronize();
@@ -909,6 +1013,7 @@ void dmsgm_destroy(dmsgm_ctx* c) {
         for (int k = 0; k < 3; ++k)
             if (c->ipc_open[side][k]) cudaIpcCloseMemHandle(c->ipc_open[side][k]);
     if (c->flags) cudaFree(c->flags);
+    if (c->pf_buf) cudaFree(c->pf_buf);
     if (c->item_ctr) cudaFree(c->item_ctr);
     if (c->status_host) cudaFreeHost(c->status_host);
     for (int i = 0; i < 2; ++i) {

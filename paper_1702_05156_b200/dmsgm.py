@@ -30,7 +30,7 @@ EXPORTS = ("dmsgm_create", "dmsgm_step", "dmsgm_step_n", "dmsgm_step_host", "dms
            "dmsgm_last_error", "dmsgm_destroy", "dmsgm_version",
            "dmsgm_set_band", "dmsgm_get_buffers", "dmsgm_attach_peer", "dmsgm_get_ipc_handles",
            "dmsgm_attach_peer_ipc", "dmsgm_band_signal", "dmsgm_band_wait", "dmsgm_band_sync",
-           "dmsgm_get_status", "dmsgm_band_halo_needed")
+           "dmsgm_get_status", "dmsgm_band_halo_needed", "dmsgm_set_prefilter", "dmsgm_prefilter")
 DMSGM_IPC_BYTES = 192
 
 
@@ -92,6 +92,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.dmsgm_band_sync.argtypes = [P, P]
     lib.dmsgm_get_status.argtypes = [P, ctypes.POINTER(ctypes.c_uint)]
     lib.dmsgm_band_halo_needed.argtypes = [i32, i32, i32, P, i32, i32, i32, ctypes.POINTER(ctypes.c_int)]
+    lib.dmsgm_set_prefilter.argtypes = [P, i32, ctypes.c_float, i32]
+    lib.dmsgm_prefilter.argtypes = [i32, i32, i32, P, sz, P, sz, i32, ctypes.c_float, i32, P]
     lib.dmsgm_version.argtypes = []
     lib.dmsgm_version.restype = ctypes.c_char_p
     return lib
@@ -223,6 +225,11 @@ class Dmsgm:
         self._check(self._lib.dmsgm_get_info(self._h, ctypes.byref(info)))
         return info
 
+    # -- preprocessing (include/dmsgm.h) ---------------------
+    def set_prefilter(self, gauss_size: int = 5, gauss_sigma: float = 1.0, median_radius: int = 1):
+        self._check(self._lib.dmsgm_set_prefilter(self._h, gauss_size, gauss_sigma, median_radius))
+        self.info = self.get_info()
+
     # -- row band (include/dmsgm.h) -------------------------------
     def set_band(self, row0: int, rows: int, halo: int):
         self._check(self._lib.dmsgm_set_band(self._h, row0, rows, halo))
@@ -264,6 +271,15 @@ class Dmsgm:
         v = ctypes.c_uint(0)
         self._check(self._lib.dmsgm_get_status(self._h, ctypes.byref(v)))
         return v.value
+
+
+def prefilter(frames, out, gauss_size: int = 5, gauss_sigma: float = 1.0, median_radius: int = 1, stream=None):
+    """Stand-alone preprocessing of uint8 CUDA frames [count][H][W] into `out` (same shape)."""
+    count, H, W = frames.shape
+    rc = _lib.dmsgm_prefilter(W, H, count, _ptr(frames), _row_pitch(frames), _ptr(out), _row_pitch(out),
+                              gauss_size, gauss_sigma, median_radius, _stream_handle(stream))
+    if rc != DMSGM_OK:
+        raise DmsgmError(rc, "dmsgm_prefilter failed")
 
 
 def band_halo_needed(width: int, height: int, block: int, homographies: np.ndarray, row0: int, rows: int) -> int:
