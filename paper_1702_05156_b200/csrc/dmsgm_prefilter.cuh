@@ -110,25 +110,19 @@ __global__ void __launch_bounds__(kPfThreads) dmsgm_prefilter_kernel(const Prefi
     const int x0 = blockIdx.x * kPfTileX, y0 = blockIdx.y * kPfTileY, s = blockIdx.z;
     const uint8_t* in = a.in + (long long)s * a.in_stride;
 
-    // 1. input rows y0-R .. y0+32+R (clamped, R32): a warp per row, a 4-pixel word per lane
-    //    (W % 4 == 0, so a word is wholly inside or wholly outside the image): lanes 0..30
-    //    load columns x0 .. x0+123, lane 31 the 4 columns left of x0, lanes 0..1 also
-    //    x0+124 .. x0+131 (the right halo; R <= 4)
-    for (int r = warp; r < T::IN_H; r += kPfThreads / 32) {
+    // 1. input rows y0-R .. y0+32+R, columns x0-4 .. x0+131 (34 words of 4 pixels per row),
+    //    clamped (R32).  W % 4 == 0, so a word is wholly inside or wholly outside the image;
+    //    an outside word repeats the nearest border pixel.
+    constexpr int WORDS = 34;
+    for (int i = threadIdx.x; i < T::IN_H * WORDS; i += kPfThreads) {
+        const int r = i / WORDS, wc = i - r * WORDS;
         const int y = min(max(y0 - R + r, 0), a.H - 1);
         const uint8_t* row = in + (long long)y * a.in_pitch;
-        const int x = lane < 31 ? x0 + 4 * lane : x0 - 4;
+        const int x = x0 - 4 + 4 * wc;
         uint32_t w;
         if (x >= 0 && x < a.W) w = __ldg(reinterpret_cast<const unsigned int*>(row + x));
         else w = 0x01010101u * row[x < 0 ? 0 : a.W - 1];
-        *reinterpret_cast<uint32_t*>(in_s + r * T::IN_PITCH + (lane < 31 ? 4 + 4 * lane : 0)) = w;
-        if (lane < 2) {
-            const int xr = x0 + kPfTileX + 4 * lane;
-            uint32_t wr;
-            if (xr < a.W) wr = __ldg(reinterpret_cast<const unsigned int*>(row + xr));
-            else wr = 0x01010101u * row[a.W - 1];
-            *reinterpret_cast<uint32_t*>(in_s + r * T::IN_PITCH + 4 + kPfTileX + 4 * lane) = wr;
-        }
+        *reinterpret_cast<uint32_t*>(in_s + r * T::IN_PITCH + 4 * wc) = w;
     }
     __syncthreads();
 
@@ -189,13 +183,21 @@ __global__ void __launch_bounds__(kPfThreads) dmsgm_prefilter_kernel(const Prefi
     if constexpr (M > 0) {
         // positions of v outside the image take their clamped value (the median clamps,
         // R32); the sources are inside the image and never written here: no race
-        const bool border = x0 == 0 || y0 == 0 || x0 + kPfTileX + M > a.W || y0 + kPfTileY + M > a.H;
-        if (border) {
-            for (int i = threadIdx.x; i < T::V_H * T::V_W; i += kPfThreads) {
-                const int r = i / T::V_W, c = i - r * T::V_W;
-                const int y = y0 - M + r, x = x0 - M + c;
-                const int yc = min(max(y, 0), a.H - 1), xc = min(max(x, 0), a.W - 1);
-                if (yc != y || xc != x) v_s[r * T::V_PITCH + c] = v_s[(yc - (y0 - M)) * T::V_PITCH + (xc - (x0 - M))];
+        // (M = 1: at most the first / last row and the first / last columns of v; rows
+        // first, then columns, so a corner takes the clamped corner value)
+        const int last_r = min(T::V_H - 1, a.H - 1 - (y0 - M)), last_c = min(T::V_W - 1, a.W - 1 - (x0 - M));
+        if (y0 == 0 || last_r < T::V_H - 1) {
+            for (int c = threadIdx.x; c < T::V_W; c += kPfThreads) {
+                if (y0 == 0) v_s[c] = v_s[T::V_PITCH + c];
+                for (int r = last_r + 1; r < T::V_H; ++r) v_s[r * T::V_PITCH + c] = v_s[last_r * T::V_PITCH + c];
+            }
+            __syncthreads();
+        }
+        if (x0 == 0 || last_c < T::V_W - 1) {
+            for (int r = threadIdx.x; r < T::V_H; r += kPfThreads) {
+                uint8_t* row = v_s + r * T::V_PITCH;
+                if (x0 == 0) row[0] = row[1];
+                for (int c = last_c + 1; c < T::V_W; ++c) row[c] = row[last_c];
             }
             __syncthreads();
         }
