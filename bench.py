@@ -68,6 +68,15 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def ncu_instructions(name):
+    """warp-instructions per launch of a kernel from the committed ncu capture (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_instr_{name}.json")) as f:
+            return float(json.load(f)["warp_instructions_per_launch"])
+    except Exception:
+        return None
+
+
 def ncu_traffic(workload):
     """dram bytes per launch from the committed ncu --set full capture (profiles/), or None."""
     path = os.path.join(ROOT, "profiles", f"ncu_traffic_{workload}.json")
@@ -345,10 +354,36 @@ def run_dmsgm(args, rank, world, local):
                          f"{wall:.1f} s wall, one single-threaded oracle step per stream per thread"}
 
     clocks = sampler.summary()
+    # NEXT-2 preprocessing: its kernel dominates the step and is ALU-bound -- time it
+    # alone (CUDA events on the launching stream) for the roofline below
+    pf_roof = None
+    if pf:
+        scratch = torch.empty_like(frames[0])
+        for i in range(3):
+            dm.prefilter(frames[i % RING], scratch, *pf, stream=stream)
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kpf = max(10, min(args.steps, 200))
+        p0.record(stream)
+        for i in range(kpf):
+            dm.prefilter(frames[i % RING], scratch, *pf, stream=stream)
+        p1.record(stream)
+        p1.synchronize()
+        pf_ms = p0.elapsed_time(p1) / kpf
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965
+        peak_issue = sms * 4 * mhz * 1e6 / 1e9          # warp-instructions / ns (4 schedulers per SM)
+        instr = ncu_instructions(f"prefilter_{args.config}")
+        pf_roof = {"bound": "alu", "unit": "G warp-inst/s", "peak": peak_issue,
+                   "achieved": instr / (pf_ms * 1e-3) / 1e9 if instr else None,
+                   "frac": instr / (pf_ms * 1e-3) / 1e9 / peak_issue if instr else None,
+                   "traffic": None, "kernel": "dmsgm_prefilter_kernel", "ms_per_launch": pf_ms,
+                   "share_of_step": pf_ms / ms_per_step, "instructions_per_launch": instr,
+                   "peak_source": f"{sms} SMs x 4 schedulers x 1 warp-instruction/clock x {mhz:.0f} MHz "
+                                  "(DESIGN.md §6.4)"}
     kernel_name = info.kernel.decode()
     ctx.close()
     if rank == 0:
-        traffic = ncu_traffic(args.config)
+        traffic = ncu_traffic(args.config) if not pf else None
         line = {
             "metric": "frames/s", "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -373,6 +408,11 @@ def run_dmsgm(args, rank, world, local):
             "gpu_launches": info.kernels_per_step * args.steps,
             "clocks": clocks,
         }
+        if pf_roof:
+            # the dominant kernel of this step is the (ALU-bound) filter; the HBM figure of
+            # the whole step is kept as roofline_step
+            line["roofline_step"] = line["roofline"]
+            line["roofline"] = pf_roof
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
