@@ -42,3 +42,40 @@ def test_fullsize_sampled_streams(cuda_lib, oracle_mod, name, T, sample, monkeyp
         compare_masks(gm[sample], om, seq.frames[t], (ost[:, 0], ost[:, 1]), N, where=f"{name} t={t}")
     ctx.close()
     o.close()
+
+
+def test_fullsize_c5b_bands(cuda_lib, oracle_mod, monkeypatch):
+    """C5b: one 4K stream split into 8 row bands (34 x 6 + 33 x 2 block rows) on concurrent
+    CUDA streams, through per-band CUDA graphs -- the bench's configuration -- equals the
+    whole-frame oracle on every frame."""
+    monkeypatch.delenv("DMSGM_KERNEL", raising=False)
+    import torch
+
+    from paper_1702_05156_b200.band import BandGroup, band_rows, halo_for
+    dm = cuda_lib
+    cfg = synth.config("C5b", T=3)
+    seq = synth.generate(cfg)
+    W, H, N, G, T = cfg.W, cfg.H, cfg.N, 8, cfg.T
+    bands = band_rows(H // N, G)
+    halo = halo_for(W, H, N, seq.homographies.reshape(-1, 9), bands)
+    pg, po = params_pair(dm, oracle_mod, 1)
+    dev = torch.device("cuda", 0)
+    streams = [torch.cuda.Stream(dev) for _ in range(G)]
+    grp = BandGroup(W, H, N, pg, G, halo, streams=streams)
+    fb = [torch.from_numpy(np.ascontiguousarray(seq.frames[:, :, b.row0 * N:b.row1 * N])).to(dev) for b in bands]
+    mb = [torch.zeros_like(f) for f in fb]
+    h = torch.from_numpy(np.ascontiguousarray(seq.homographies)).to(dev)
+    torch.cuda.synchronize()
+    grp.step_n(T, fb, h, mb)
+    torch.cuda.synchronize()
+    assert grp.status() == [0] * G
+    gm = np.concatenate([m.cpu().numpy() for m in mb], axis=2)          # [T][1][H][W]
+    gst = grp.get_state(0)
+    grp.close()
+    om, ost = oracle_mod.Oracle(W, H, N, po), None
+    for t in range(T):
+        o_mask = om.step(seq.frames[t], seq.homographies[t])
+        ost = np.stack([om.get_state(0)])
+        compare_masks(gm[t], o_mask, seq.frames[t], (ost[:, 0], ost[:, 1]), N, where=f"C5b t={t}")
+    compare_state(gst[None], ost, where="C5b final")
+    om.close()
