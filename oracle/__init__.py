@@ -21,6 +21,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dmsgm_oracle.c")
 _SRC2 = os.path.join(_HERE, "prefilter_oracle.c")
+_SRC3 = os.path.join(_HERE, "warp_oracle.c")
 _HDR = os.path.join(_HERE, "dmsgm_oracle.h")
 LIB_PATH = os.path.join(_HERE, "libdmsgm_oracle.so")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
@@ -32,10 +33,10 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile the oracle into oracle/libdmsgm_oracle.so (gcc, no FMA contraction)."""
-    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC2), os.path.getmtime(_HDR))
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC2), os.path.getmtime(_SRC3), os.path.getmtime(_HDR))
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
         tmp = LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC2, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC2, _SRC3, "-lm"])
         os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
@@ -72,6 +73,7 @@ def _load():
             lib.dmsgm_oracle_decay_exp.restype = ctypes.c_float
             lib.dmsgm_oracle_gauss_taps.argtypes = [i32, ctypes.c_float, P]
             lib.dmsgm_oracle_prefilter.argtypes = [i32, i32, P, sz, P, sz, i32, ctypes.c_float, i32]
+            lib.dmsgm_oracle_warp_frame.argtypes = [i32, i32, P, sz, P, P, sz]
             _lib = lib
     return _lib
 
@@ -198,6 +200,28 @@ def prefilter_frames(frames: np.ndarray, gauss_size: int = 5, gauss_sigma: float
     flat_out = out.reshape(-1, *frames.shape[-2:])
     for i in range(flat_in.shape[0]):
         flat_out[i] = prefilter(flat_in[i], gauss_size, gauss_sigma, median_radius)
+    return out
+
+
+def warp_frame(frame: np.ndarray, h) -> np.ndarray:
+    """App. F frame-warp motion compensation of one u8 frame [H][W] (readings R35-R37)."""
+    f = np.ascontiguousarray(frame, np.uint8)
+    hh = np.ascontiguousarray(np.asarray(h, np.float64).reshape(9))
+    Hh, W = f.shape
+    out = np.empty_like(f)
+    if _load().dmsgm_oracle_warp_frame(W, Hh, _ptr(f), W, _ptr(hh), _ptr(out), W) != 0:
+        raise ValueError("bad warp arguments")
+    return out
+
+
+def warp_frames(frames: np.ndarray, homographies: np.ndarray) -> np.ndarray:
+    """warp_frame over [..., H, W] frames with [..., 9] homographies."""
+    out = np.empty_like(frames)
+    fi = frames.reshape(-1, *frames.shape[-2:])
+    hi = homographies.reshape(-1, 9)
+    fo = out.reshape(-1, *frames.shape[-2:])
+    for i in range(fi.shape[0]):
+        fo[i] = warp_frame(fi[i], hi[i])
     return out
 
 

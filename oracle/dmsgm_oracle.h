@@ -81,6 +81,12 @@ int dmsgm_oracle_gauss_taps(int size, float sigma, float* taps);
 int dmsgm_oracle_prefilter(int width, int height, const uint8_t* in, size_t in_pitch, uint8_t* out,
                            size_t out_pitch, int gauss_size, float gauss_sigma, int median_radius);
 
+/* Frame-warp motion compensation of App. F (warp_oracle.c, readings R35-R37): out
+ * samples `in` (frame t) at H^-1 of every pixel centre, H = h[9] the step's homography
+ * (frame t -> frame t-1, R3); bilinear, border pixels repeated. */
+int dmsgm_oracle_warp_frame(int width, int height, const uint8_t* in, size_t in_pitch, const double* h,
+                            uint8_t* out, size_t out_pitch);
+
 #ifdef __cplusplus
 }
 #endif
