@@ -149,7 +149,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (test infrastructure; the only other place bench.py runs oracle/)
 # ---------------------------------------------------------------------------
-def oracle_throughput(cfg, frames_host, Hs, n_streams, n_frames, threads, prefilter=None):
+def oracle_throughput(cfg, frames_host, Hs, n_streams, n_frames, threads, prefilter=None, frame_warp=False):
     """Oracle frames/s on `n_streams` streams x `n_frames` frames, one thread per stream
     (ctypes releases the GIL; the oracle itself is single-threaded).  Returns (fps, cores, wall)."""
     import oracle
@@ -162,9 +162,13 @@ def oracle_throughput(cfg, frames_host, Hs, n_streams, n_frames, threads, prefil
     def run_frame(t):
         def one(s):
             fr = frames_host[t % R, s % frames_host.shape[1]]
+            h = Hs[t % R, s % Hs.shape[1]]
             if prefilter:
                 fr = oracle.prefilter(fr, *prefilter)
-            o.step_stream(s, fr, Hs[t % R, s % Hs.shape[1]], masks[s])
+            if frame_warp:                       # App. F: warp the frame, then the step with H = I
+                fr = oracle.warp_frame(fr, h)
+                h = np.eye(3).reshape(9)
+            o.step_stream(s, fr, h, masks[s])
         with ThreadPoolExecutor(max_workers=threads) as ex:
             list(ex.map(one, range(n_streams)))
         o.commit()
@@ -274,6 +278,8 @@ def run_dmsgm(args, rank, world, local):
         gs, sg, mr = args.prefilter.split(",")
         pf = (int(gs), float(sg), int(mr))
         ctx.set_prefilter(*pf)                  # Gaussian + median before the step
+    if args.motion == "frame":
+        ctx.set_motion(dm.DMSGM_MC_FRAME)       # App. F frame warp, models not warped
     info = ctx.info
     stream = torch.cuda.current_stream(dev)
     bytes_per_step = S * info.algorithmic_bytes_per_frame
@@ -348,7 +354,8 @@ def run_dmsgm(args, rank, world, local):
         if pf:
             per_frame += 0.15 * (W * H) / (1920 * 1080)                      # + the oracle's filters
         nf = max(2, int(target_s / per_frame / ns * min(cores, ns)))
-        cfps, used, wall = oracle_throughput(cfg, fh, Hs[:2, :ns], ns, nf, cores, prefilter=pf)
+        cfps, used, wall = oracle_throughput(cfg, fh, Hs[:2, :ns], ns, nf, cores, prefilter=pf,
+                                             frame_warp=args.motion == "frame")
         cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle",
                "sample": f"{ns} streams x {nf} frames of {wl['desc'].split(',')[0]} (N={N}), "
                          f"{wall:.1f} s wall, one single-threaded oracle step per stream per thread"}
@@ -380,16 +387,37 @@ def run_dmsgm(args, rank, world, local):
                    "share_of_step": pf_ms / ms_per_step, "instructions_per_launch": instr,
                    "peak_source": f"{sms} SMs x 4 schedulers x 1 warp-instruction/clock x {mhz:.0f} MHz "
                                   "(DESIGN.md §6.4)"}
+    warp_roof = None
+    if args.motion == "frame":
+        # the frame-warp kernel alone (CUDA events on the launching stream)
+        scratch = torch.empty_like(frames[0])
+        for i in range(3):
+            dm.warp_frames(frames[i % RING], Hs_dev[i % RING], scratch, stream=stream)
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kw = max(10, min(args.steps, 200))
+        p0.record(stream)
+        for i in range(kw):
+            dm.warp_frames(frames[i % RING], Hs_dev[i % RING], scratch, stream=stream)
+        p1.record(stream)
+        p1.synchronize()
+        w_ms = p0.elapsed_time(p1) / kw
+        wbytes = 2.0 * S * W * H
+        warp_roof = {"bound": "hbm", "unit": "GB/s", "peak": peak, "achieved": wbytes / (w_ms * 1e-3) / 1e9,
+                     "frac": wbytes / (w_ms * 1e-3) / 1e9 / peak, "kernel": "dmsgm_warp_kernel",
+                     "ms_per_launch": w_ms, "share_of_step": w_ms / ms_per_step,
+                     "algorithmic_bytes_per_launch": wbytes, "traffic": None}
     kernel_name = info.kernel.decode()
     ctx.close()
     if rank == 0:
-        traffic = ncu_traffic(args.config) if not pf else None
+        traffic = ncu_traffic(args.config) if not (pf or args.motion == "frame") else None
         line = {
             "metric": "frames/s", "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth/ ring recipe, generated on device)",
-            "config": {"workload": args.config + ("+prefilter" if pf else ""), "desc": wl["desc"], "W": W, "H": H,
+            "config": {"workload": args.config + ("+prefilter" if pf else "") + ("+framewarp" if args.motion == "frame"
+                                                                                   else ""),
+                       "desc": wl["desc"], "W": W, "H": H, "motion_compensation": args.motion,
                        "N": N, "prefilter": {"gauss_size": pf[0], "gauss_sigma": pf[1], "median_radius": pf[2]}
                        if pf else None,
                        "streams_per_gpu": S, "total_streams": total_streams, "ring_frames": RING,
@@ -413,6 +441,8 @@ def run_dmsgm(args, rank, world, local):
             # the whole step is kept as roofline_step
             line["roofline_step"] = line["roofline"]
             line["roofline"] = pf_roof
+        if warp_roof:
+            line["roofline_warp"] = warp_roof
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -637,6 +667,8 @@ def main():
                     help="C5b under torchrun: fused peer stores + sync kernel, or NCCL send/recv baseline")
     ap.add_argument("--prefilter", default="",
                     help="GAUSS_SIZE,SIGMA,MEDIAN_RADIUS (e.g. 5,1.0,1): NEXT-2 preprocessing before every step")
+    ap.add_argument("--motion", default="models", choices=["models", "frame"],
+                    help="motion compensation: warp the models (default, north_star) or the frame (App. F, NEXT-3)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="C5b: process-group backend (gloo + --same-device: functional test on one GPU)")
     ap.add_argument("--same-device", action="store_true", help="C5b: every rank on cuda:0 (testing only)")

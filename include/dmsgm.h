@@ -159,6 +159,28 @@ int dmsgm_prefilter(int width, int height, int count, const uint8_t* in, size_t 
                     size_t out_pitch, int gauss_size, float gauss_sigma, int median_radius, void* cuda_stream);
 
 /* ------------------------------------------------------------------------------------
+ * Motion-compensation mode.  DMSGM_MC_MODELS (default, the
+ * north_star and §2.4): the previous models are warped and mixed through H (S1-S3).
+ * DMSGM_MC_FRAME: the paper's own code path (App. F, warpPerspective with
+ * INTER_LINEAR | WARP_INVERSE_MAP; §3.1.3): the current frame is resampled into the
+ * previous frame's coordinates (bilinear, borders repeated; R35-R37) and the
+ * models are updated in place (H = I); masks are then in the previous frame's coordinates.
+ * ------------------------------------------------------------------------------------ */
+#define DMSGM_MC_MODELS 0
+#define DMSGM_MC_FRAME  1
+
+/* Select the mode (one extra kernel per step and a warped-frame buffer of S * height *
+ * round_up(width, 16) bytes in DMSGM_MC_FRAME).  Not in row-band mode (DMSGM_ESTATE).
+ * Synchronises the device. */
+int dmsgm_set_motion(dmsgm_ctx* ctx, int mode);
+
+/* Stand-alone frame warp of `count` frames: in / out u8 [count][height][pitch] (device,
+ * width % 4 == 0, 4-byte aligned pitches and bases), homographies f64 [count][9]
+ * (device, frame t -> frame t-1 as for the step).  Enqueued on cuda_stream. */
+int dmsgm_warp_frames(int width, int height, int count, const uint8_t* in, size_t in_pitch,
+                      const double* homographies, uint8_t* out, size_t out_pitch, void* cuda_stream);
+
+/* ------------------------------------------------------------------------------------
  * Row-band split of one large frame over several GPUs (
  * north_star: "a single very large frame may optionally be split into row bands with
  * a one-block-row halo exchanged over NVLink").  Only S1-S2 read neighbouring blocks

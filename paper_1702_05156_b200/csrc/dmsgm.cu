@@ -18,6 +18,7 @@
 #include "dmsgm.h"
 #include "dmsgm_kernel.cuh"
 #include "dmsgm_prefilter.cuh"
+#include "dmsgm_warp.cuh"
 
 using namespace dmsgm;
 
@@ -79,6 +80,11 @@ struct dmsgm_ctx {
     float pf_taps[2 * kPfMaxG + 1];
     uint8_t* pf_buf;
     size_t pf_pitch;
+    // frame-warp motion compensation: warped-frame buffer
+    // ([S][H][pf_pitch-like pitch]) and S identity homographies for the step that follows
+    uint8_t* wf_buf;
+    size_t wf_pitch;
+    double* id_H;
     char err[512];
 };
 
@@ -288,6 +294,18 @@ bool gauss_taps(int size, float sigma, float* taps) {
     return true;
 }
 
+cudaError_t launch_warp(int W, int H, int count, const uint8_t* in, long long in_stride, size_t in_pitch,
+                        const double* Hs, uint8_t* out, long long out_stride, size_t out_pitch, cudaStream_t stream) {
+    WarpArgs a;
+    a.in = in; a.in_stride = in_stride; a.in_pitch = (int)in_pitch;
+    a.out = out; a.out_stride = out_stride; a.out_pitch = (int)out_pitch;
+    a.H = Hs; a.W = W; a.Hh = H;
+    const dim3 block(kWarpThreadsX, kWarpRows, 1);
+    const dim3 grid((W / 4 + kWarpThreadsX - 1) / kWarpThreadsX, (H + kWarpRows - 1) / kWarpRows, count);
+    dmsgm_warp_kernel<<<grid, block, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_prefilter(int W, int H, int count, const uint8_t* in, long long in_stride, size_t in_pitch,
                              uint8_t* out, long long out_stride, size_t out_pitch, int g, int m, const float* taps,
                              cudaStream_t stream) {
@@ -331,6 +349,17 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
         if (e != cudaSuccess) return e;
         frames = pf;
         fpitch = c->pf_pitch;
+    }
+    if (c->wf_buf) {
+        // frame-warp motion compensation (R35): frame t resampled into frame t-1's
+        // coordinates, then the step with H = I (the models are not warped)
+        uint8_t* wf = c->wf_buf + (size_t)s0 * c->Hp * c->wf_pitch;
+        cudaError_t e = launch_warp(c->W, c->Hp, count, frames, (long long)c->Hp * fpitch, fpitch, H, wf,
+                                    (long long)c->Hp * c->wf_pitch, c->wf_pitch, stream);
+        if (e != cudaSuccess) return e;
+        frames = wf;
+        fpitch = c->wf_pitch;
+        H = c->id_H + (size_t)s0 * 9;
     }
     StepArgs a;
     a.frames = frames;
@@ -733,7 +762,7 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     if (!c || !out) return DMSGM_EINVAL;
     out->width = c->W; out->height = c->H; out->block = c->N;
     out->blocks_x = c->Wb; out->blocks_y = c->Hb; out->num_streams = c->S;
-    out->kernels_per_step = (has_peers(c) ? 2 : 1) + (c->pf_buf ? 1 : 0);
+    out->kernels_per_step = (has_peers(c) ? 2 : 1) + (c->pf_buf ? 1 : 0) + (c->wf_buf ? 1 : 0);
     out->band_row0 = c->row0; out->band_rows = c->rows; out->band_halo = c->halo;
     out->state_bytes = (size_t)c->S * stream_floats(c) * sizeof(float);
     // frame read (1 B/px) + mask write (1 B/px) + state read + write (2 x 24 B per block)
@@ -743,6 +772,7 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
                                        24.0 * (double)c->Wb * c->halo * nb;
     // preprocessing as its own kernel: + read the frame + write the filtered frame
     if (c->pf_buf) out->algorithmic_bytes_per_frame += 2.0 * c->W * c->Hp;
+    if (c->wf_buf) out->algorithmic_bytes_per_frame += 2.0 * c->W * c->Hp;     // frame warp: read + write
     if (c->staged)
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d> (TMA, persistent)", c->N,
                  c->N == 8 ? 1 : 2, c->staged_occ);
@@ -797,6 +827,56 @@ int dmsgm_set_prefilter(dmsgm_ctx* c, int gauss_size, float gauss_sigma, int med
     return DMSGM_OK;
 }
 
+// ---- frame-warp motion compensation ----
+
+int dmsgm_warp_frames(int width, int height, int count, const uint8_t* in, size_t in_pitch,
+                      const double* homographies, uint8_t* out, size_t out_pitch, void* stream) {
+    if (!in || !out || !homographies || width < 4 || width % 4 || height < 1 || count < 1 ||
+        in_pitch < (size_t)width || out_pitch < (size_t)width || (in_pitch & 3) || (out_pitch & 3) ||
+        ((uintptr_t)in & 3) || ((uintptr_t)out & 3) || ((uintptr_t)homographies & 7))
+        return DMSGM_EINVAL;
+    cudaError_t e = launch_warp(width, height, count, in, (long long)height * in_pitch, in_pitch, homographies, out,
+                                (long long)height * out_pitch, out_pitch, (cudaStream_t)stream);
+    return e == cudaSuccess ? DMSGM_OK : DMSGM_ECUDA;
+}
+
+int dmsgm_set_motion(dmsgm_ctx* c, int mode) {
+    if (!c) return DMSGM_EINVAL;
+    if (mode != DMSGM_MC_MODELS && mode != DMSGM_MC_FRAME)
+        return fail(c, DMSGM_EINVAL, "mode must be DMSGM_MC_MODELS (0) or DMSGM_MC_FRAME (1)");
+    if (mode == DMSGM_MC_FRAME && c->band) return fail(c, DMSGM_ESTATE, "frame warping is not supported in row-band mode");
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_set_motion sync");
+    destroy_graphs(c);
+    if (mode == DMSGM_MC_MODELS) {
+        if (c->wf_buf) cudaFree(c->wf_buf);
+        if (c->id_H) cudaFree(c->id_H);
+        c->wf_buf = nullptr;
+        c->id_H = nullptr;
+        return DMSGM_OK;
+    }
+    if (!c->wf_buf) {
+        c->wf_pitch = ((size_t)c->W + 15) & ~(size_t)15;
+        double* hid = (double*)malloc((size_t)c->S * 9 * sizeof(double));
+        if (!hid) return fail(c, DMSGM_ENOMEM, "host allocation failed");
+        for (int s = 0; s < c->S; ++s)
+            for (int i = 0; i < 9; ++i) hid[9 * s + i] = (i % 4 == 0) ? 1.0 : 0.0;
+        if ((e = cudaMalloc(&c->wf_buf, (size_t)c->S * c->H * c->wf_pitch)) != cudaSuccess ||
+            (e = cudaMalloc(&c->id_H, (size_t)c->S * 9 * sizeof(double))) != cudaSuccess ||
+            (e = cudaMemcpy(c->id_H, hid, (size_t)c->S * 9 * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess) {
+            free(hid);
+            if (c->wf_buf) cudaFree(c->wf_buf);
+            if (c->id_H) cudaFree(c->id_H);
+            c->wf_buf = nullptr;
+            c->id_H = nullptr;
+            return fail(c, DMSGM_ENOMEM, "warped-frame buffer: %s", cudaGetErrorString(e));
+        }
+        free(hid);
+    }
+    return DMSGM_OK;
+}
+
 // ---- row band ----
 
 namespace {
@@ -825,8 +905,8 @@ int dmsgm_set_band(dmsgm_ctx* c, int row0, int rows, int halo) {
     if (row0 < 0 || rows < 1 || row0 + rows > c->Hb)
         return fail(c, DMSGM_EINVAL, "band rows [%d, %d) outside [0, %d)", row0, row0 + rows, c->Hb);
     if (halo < 0 || halo > rows) return fail(c, DMSGM_EINVAL, "halo must be in [0, rows]");
-    if (c->pf_buf && !(row0 == 0 && rows == c->Hb && halo == 0))
-        return fail(c, DMSGM_ESTATE, "preprocessing is not supported in row-band mode");
+    if ((c->pf_buf || c->wf_buf) && !(row0 == 0 && rows == c->Hb && halo == 0))
+        return fail(c, DMSGM_ESTATE, "preprocessing / frame warping is not supported in row-band mode");
     DeviceGuard g(c->device);
     if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
     cudaError_t e = cudaDeviceSynchronize();
@@ -1014,6 +1094,8 @@ void dmsgm_destroy(dmsgm_ctx* c) {
             if (c->ipc_open[side][k]) cudaIpcCloseMemHandle(c->ipc_open[side][k]);
     if (c->flags) cudaFree(c->flags);
     if (c->pf_buf) cudaFree(c->pf_buf);
+    if (c->wf_buf) cudaFree(c->wf_buf);
+    if (c->id_H) cudaFree(c->id_H);
     if (c->item_ctr) cudaFree(c->item_ctr);
     if (c->status_host) cudaFreeHost(c->status_host);
     for (int i = 0; i < 2; ++i) {

@@ -30,7 +30,10 @@ EXPORTS = ("dmsgm_create", "dmsgm_step", "dmsgm_step_n", "dmsgm_step_host", "dms
            "dmsgm_last_error", "dmsgm_destroy", "dmsgm_version",
            "dmsgm_set_band", "dmsgm_get_buffers", "dmsgm_attach_peer", "dmsgm_get_ipc_handles",
            "dmsgm_attach_peer_ipc", "dmsgm_band_signal", "dmsgm_band_wait", "dmsgm_band_sync",
-           "dmsgm_get_status", "dmsgm_band_halo_needed", "dmsgm_set_prefilter", "dmsgm_prefilter")
+           "dmsgm_get_status", "dmsgm_band_halo_needed", "dmsgm_set_prefilter", "dmsgm_prefilter",
+           "dmsgm_set_motion", "dmsgm_warp_frames")
+DMSGM_MC_MODELS = 0
+DMSGM_MC_FRAME = 1
 DMSGM_IPC_BYTES = 192
 
 
@@ -93,6 +96,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.dmsgm_get_status.argtypes = [P, ctypes.POINTER(ctypes.c_uint)]
     lib.dmsgm_band_halo_needed.argtypes = [i32, i32, i32, P, i32, i32, i32, ctypes.POINTER(ctypes.c_int)]
     lib.dmsgm_set_prefilter.argtypes = [P, i32, ctypes.c_float, i32]
+    lib.dmsgm_set_motion.argtypes = [P, i32]
+    lib.dmsgm_warp_frames.argtypes = [i32, i32, i32, P, sz, P, P, sz, P]
     lib.dmsgm_prefilter.argtypes = [i32, i32, i32, P, sz, P, sz, i32, ctypes.c_float, i32, P]
     lib.dmsgm_version.argtypes = []
     lib.dmsgm_version.restype = ctypes.c_char_p
@@ -230,6 +235,11 @@ class Dmsgm:
         self._check(self._lib.dmsgm_set_prefilter(self._h, gauss_size, gauss_sigma, median_radius))
         self.info = self.get_info()
 
+    def set_motion(self, mode: int):
+        """DMSGM_MC_MODELS (0, default) or DMSGM_MC_FRAME (1, App. F frame warp)."""
+        self._check(self._lib.dmsgm_set_motion(self._h, mode))
+        self.info = self.get_info()
+
     # -- row band (include/dmsgm.h, SURVEY §8(e)) -------------------------------
     def set_band(self, row0: int, rows: int, halo: int):
         self._check(self._lib.dmsgm_set_band(self._h, row0, rows, halo))
@@ -280,6 +290,15 @@ def prefilter(frames, out, gauss_size: int = 5, gauss_sigma: float = 1.0, median
                               gauss_size, gauss_sigma, median_radius, _stream_handle(stream))
     if rc != DMSGM_OK:
         raise DmsgmError(rc, "dmsgm_prefilter failed")
+
+
+def warp_frames(frames, homographies, out, stream=None):
+    """Stand-alone App. F frame warp of uint8 CUDA frames [count][H][W] into `out`."""
+    count, H, W = frames.shape
+    rc = _lib.dmsgm_warp_frames(W, H, count, _ptr(frames), _row_pitch(frames), _ptr(homographies), _ptr(out),
+                                _row_pitch(out), _stream_handle(stream))
+    if rc != DMSGM_OK:
+        raise DmsgmError(rc, "dmsgm_warp_frames failed")
 
 
 def band_halo_needed(width: int, height: int, block: int, homographies: np.ndarray, row0: int, rows: int) -> int:
