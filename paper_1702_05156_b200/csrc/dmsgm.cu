@@ -301,7 +301,7 @@ cudaError_t launch_warp(int W, int H, int count, const uint8_t* in, long long in
     a.out = out; a.out_stride = out_stride; a.out_pitch = (int)out_pitch;
     a.H = Hs; a.W = W; a.Hh = H;
     const dim3 block(kWarpThreadsX, kWarpRows, 1);
-    const dim3 grid((W / 4 + kWarpThreadsX - 1) / kWarpThreadsX, (H + kWarpRows - 1) / kWarpRows, count);
+    const dim3 grid((W / 4 + kWarpThreadsX - 1) / kWarpThreadsX, (H + kWarpTileY - 1) / kWarpTileY, count);
     dmsgm_warp_kernel<<<grid, block, 0, stream>>>(a);
     return cudaGetLastError();
 }
