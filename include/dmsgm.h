@@ -111,6 +111,16 @@ int dmsgm_step_host(dmsgm_ctx* ctx, const uint8_t* host_frames, size_t frame_pit
                     const double* host_homographies, uint8_t* host_masks, size_t mask_pitch,
                     void* cuda_stream);
 
+/* The same, ASYNCHRONOUS: returns after enqueueing.  Consecutive async calls pipeline
+ * (step t+1's uploads overlap step t's kernels and downloads; each chunk of streams
+ * follows its own previous chunk); work enqueued later on `cuda_stream`, and a sync of
+ * it, sees the step complete.  It does NOT wait for earlier work on `cuda_stream` (its
+ * inputs are host memory).  host_frames / host_homographies must stay unchanged and
+ * host_masks unread until then. */
+int dmsgm_step_host_async(dmsgm_ctx* ctx, const uint8_t* host_frames, size_t frame_pitch,
+                          const double* host_homographies, uint8_t* host_masks, size_t mask_pitch,
+                          void* cuda_stream);
+
 /* Mark stream `stream` (or all, -1) fresh: its next step re-initialises (R8).
  * Synchronises the device first. */
 int dmsgm_reset(dmsgm_ctx* ctx, int stream);

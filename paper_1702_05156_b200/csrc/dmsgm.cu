@@ -57,6 +57,7 @@ struct dmsgm_ctx {
     double* st_H;
     cudaStream_t pipe[kPipeStreams];
     cudaEvent_t ev_start;
+    cudaEvent_t ev_done[kPipeStreams];   // dmsgm_step_host_async: end of each pipe stream's work
     bool pipe_ready;
     int staged;        // 1: persistent TMA-staged kernel (N = 4, N = 8)
     int staged_ctas;   // resident CTAs of the staged kernel on this device
@@ -629,8 +630,9 @@ int dmsgm_step_n(dmsgm_ctx* c, int T, const uint8_t* frames, size_t fpitch, cons
     return DMSGM_OK;
 }
 
-int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double* hH, uint8_t* hm,
-                    size_t mpitch, void* cuda_stream) {
+namespace {
+int step_host_impl(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double* hH, uint8_t* hm, size_t mpitch,
+                   void* cuda_stream, bool async) {
     if (!c) return DMSGM_EINVAL;
     if (!hf || !hH || !hm) return fail(c, DMSGM_EINVAL, "null host pointer");
     if (fpitch < (size_t)c->W || mpitch < (size_t)c->W)
@@ -652,11 +654,19 @@ int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double
                 return cuda_fail(c, e, "cudaStreamCreate");
         if ((e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming)) != cudaSuccess)
             return cuda_fail(c, e, "cudaEventCreate");
+        for (int i = 0; i < kPipeStreams; ++i)
+            if ((e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(c, e, "cudaEventCreate");
         c->pipe_ready = true;
     }
-    if ((e = cudaEventRecord(c->ev_start, (cudaStream_t)cuda_stream)) != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
-    for (int i = 0; i < kPipeStreams; ++i)
-        if ((e = cudaStreamWaitEvent(c->pipe[i], c->ev_start, 0)) != cudaSuccess) return cuda_fail(c, e, "cudaStreamWaitEvent");
+    if (!async) {
+        // ordered after the caller's earlier work on cuda_stream
+        if ((e = cudaEventRecord(c->ev_start, (cudaStream_t)cuda_stream)) != cudaSuccess)
+            return cuda_fail(c, e, "cudaEventRecord");
+        for (int i = 0; i < kPipeStreams; ++i)
+            if ((e = cudaStreamWaitEvent(c->pipe[i], c->ev_start, 0)) != cudaSuccess)
+                return cuda_fail(c, e, "cudaStreamWaitEvent");
+    }
     // chunks of streams: H2D(k) || kernel(k-1) || D2H(k-2) across the pipe streams
     const char* cenv = getenv("DMSGM_HOST_CHUNKS");
     int nchunks = cenv ? atoi(cenv) : 8;
@@ -683,11 +693,32 @@ int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double
                                    cudaMemcpyDeviceToHost, st)) != cudaSuccess)
             return cuda_fail(c, e, "D2H masks");
     }
-    for (int i = 0; i < kPipeStreams; ++i)
-        if ((e = cudaStreamSynchronize(c->pipe[i])) != cudaSuccess) return cuda_fail(c, e, "dmsgm_step_host sync");
+    if (async) {
+        // work enqueued later on cuda_stream (and a sync on it) sees this step complete;
+        // the next async step's chunk k follows this one's chunk k on the same pipe stream
+        for (int i = 0; i < kPipeStreams; ++i) {
+            if ((e = cudaEventRecord(c->ev_done[i], c->pipe[i])) != cudaSuccess ||
+                (e = cudaStreamWaitEvent((cudaStream_t)cuda_stream, c->ev_done[i], 0)) != cudaSuccess)
+                return cuda_fail(c, e, "dmsgm_step_host_async events");
+        }
+    } else {
+        for (int i = 0; i < kPipeStreams; ++i)
+            if ((e = cudaStreamSynchronize(c->pipe[i])) != cudaSuccess) return cuda_fail(c, e, "dmsgm_step_host sync");
+    }
     c->cur ^= 1;
     c->steps += 1;
     return DMSGM_OK;
+}
+}  // namespace
+
+int dmsgm_step_host(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double* hH, uint8_t* hm,
+                    size_t mpitch, void* cuda_stream) {
+    return step_host_impl(c, hf, fpitch, hH, hm, mpitch, cuda_stream, false);
+}
+
+int dmsgm_step_host_async(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double* hH, uint8_t* hm,
+                          size_t mpitch, void* cuda_stream) {
+    return step_host_impl(c, hf, fpitch, hH, hm, mpitch, cuda_stream, true);
 }
 
 int dmsgm_reset(dmsgm_ctx* c, int stream) {
@@ -1104,7 +1135,10 @@ void dmsgm_destroy(dmsgm_ctx* c) {
     }
     if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
     if (c->pipe_ready) {
-        for (int i = 0; i < kPipeStreams; ++i) cudaStreamDestroy(c->pipe[i]);
+        for (int i = 0; i < kPipeStreams; ++i) {
+            cudaStreamDestroy(c->pipe[i]);
+            cudaEventDestroy(c->ev_done[i]);
+        }
         cudaEventDestroy(c->ev_start);
     }
     if (c->st_frames) cudaFree(c->st_frames);

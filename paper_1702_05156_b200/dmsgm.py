@@ -25,7 +25,7 @@ DMSGM_ESTATE = -4
 _ERRNAMES = {-1: "DMSGM_EINVAL", -2: "DMSGM_ENOMEM", -3: "DMSGM_ECUDA", -4: "DMSGM_ESTATE"}
 
 # Every symbol include/dmsgm.h declares (checked by tests/test_abi.py).
-EXPORTS = ("dmsgm_create", "dmsgm_step", "dmsgm_step_n", "dmsgm_step_host", "dmsgm_reset",
+EXPORTS = ("dmsgm_create", "dmsgm_step", "dmsgm_step_n", "dmsgm_step_host", "dmsgm_step_host_async", "dmsgm_reset",
            "dmsgm_get_state", "dmsgm_set_state", "dmsgm_is_initialised", "dmsgm_get_info",
            "dmsgm_last_error", "dmsgm_destroy", "dmsgm_version",
            "dmsgm_set_band", "dmsgm_get_buffers", "dmsgm_attach_peer", "dmsgm_get_ipc_handles",
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.dmsgm_step.argtypes = [P, P, sz, P, P, sz, P]
     lib.dmsgm_step_n.argtypes = [P, i32, P, sz, P, P, sz, P]
     lib.dmsgm_step_host.argtypes = [P, P, sz, P, P, sz, P]
+    lib.dmsgm_step_host_async.argtypes = [P, P, sz, P, P, sz, P]
     lib.dmsgm_reset.argtypes = [P, i32]
     lib.dmsgm_get_state.argtypes = [P, i32, P]
     lib.dmsgm_set_state.argtypes = [P, i32, P]
@@ -208,6 +209,11 @@ class Dmsgm:
         """HOST buffers (numpy or pinned CPU tensors); synchronous."""
         self._check(self._lib.dmsgm_step_host(self._h, _ptr(frames), _row_pitch(frames), _ptr(homographies),
                                               _ptr(masks), _row_pitch(masks), _stream_handle(stream)))
+
+    def step_host_async(self, frames, homographies, masks, stream=None):
+        """HOST buffers (pinned); returns after enqueueing (see include/dmsgm.h)."""
+        self._check(self._lib.dmsgm_step_host_async(self._h, _ptr(frames), _row_pitch(frames), _ptr(homographies),
+                                                    _ptr(masks), _row_pitch(masks), _stream_handle(stream)))
 
     def reset(self, stream: int = -1):
         self._check(self._lib.dmsgm_reset(self._h, stream))

@@ -157,6 +157,30 @@ def test_step_host_equals_oracle(cuda_lib, oracle_mod, kernel_path):
     _check_run(cuda_lib, oracle_mod, seq.frames, seq.homographies, cfg.N, pg, po, mode="host")
 
 
+def test_step_host_async_pipelined(cuda_lib, oracle_mod):
+    """dmsgm_step_host_async: T steps enqueued back to back (chunks of consecutive steps
+    overlap on the pipe streams), one sync at the end; every step's masks and the final
+    state equal the oracle's."""
+    import torch
+    cfg = synth.config("C4", W=320, H=240, T=6, S=11)
+    seq = synth.generate(cfg)
+    pg, po = params_pair(cuda_lib, oracle_mod, cfg.S)
+    T, S, H, W = seq.frames.shape
+    ctx = cuda_lib.Dmsgm(W, H, cfg.N, pg)
+    hf = [torch.from_numpy(np.ascontiguousarray(seq.frames[t])).pin_memory() for t in range(T)]
+    hh = [torch.from_numpy(np.ascontiguousarray(seq.homographies[t])).pin_memory() for t in range(T)]
+    hm = [torch.zeros((S, H, W), dtype=torch.uint8).pin_memory() for _ in range(T)]
+    for t in range(T):
+        ctx.step_host_async(hf[t], hh[t], hm[t])
+    torch.cuda.synchronize()
+    gst = np.stack([ctx.get_state(s) for s in range(S)])
+    ctx.close()
+    om, os_ = run_oracle(oracle_mod, seq.frames, seq.homographies, cfg.N, po, snapshot_every=1)
+    for t in range(T):
+        compare_masks(hm[t].numpy(), om[t], seq.frames[t], (os_[t][:, 0], os_[t][:, 1]), cfg.N, where=f"t={t}")
+    compare_state(gst, os_[T - 1], where="final")
+
+
 def test_batch_invariance(cuda_lib, oracle_mod):
     """A stream's results do not depend on the batch it is processed in (bitwise)."""
     cfg = synth.config("C4", W=256, H=128, T=6, S=6)
