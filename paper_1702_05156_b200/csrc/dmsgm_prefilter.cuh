@@ -84,7 +84,7 @@ struct PfTile {
     static constexpr int IN_H = kPfTileY + 2 * R;         // input tile rows
     // input tile columns: x0 - 4 .. x0 + 128 + 4 (+ slack), so the tile's first column x0
     // sits on a 4-byte boundary: smem column j <-> image column x0 - 4 + j
-    static constexpr int IN_PITCH = 144;
+    static constexpr int IN_PITCH = 160;                  // 10 chunks of 16 bytes (see the load)
     static constexpr int V_W = kPfTileX + 2 * M;          // Gaussian output columns (median halo)
     static constexpr int V_H = kPfTileY + 2 * M;
     static constexpr int H_PITCH = 128;                   // floats per row-pass row: 32 groups of 4
@@ -110,19 +110,37 @@ __global__ void __launch_bounds__(kPfThreads) dmsgm_prefilter_kernel(const Prefi
     const int x0 = blockIdx.x * kPfTileX, y0 = blockIdx.y * kPfTileY, s = blockIdx.z;
     const uint8_t* in = a.in + (long long)s * a.in_stride;
 
-    // 1. input rows y0-R .. y0+32+R, columns x0-4 .. x0+131 (34 words of 4 pixels per row),
-    //    clamped (R32).  W % 4 == 0, so a word is wholly inside or wholly outside the image;
-    //    an outside word repeats the nearest border pixel.
-    constexpr int WORDS = 34;
-    for (int i = threadIdx.x; i < T::IN_H * WORDS; i += kPfThreads) {
-        const int r = i / WORDS, wc = i - r * WORDS;
-        const int y = min(max(y0 - R + r, 0), a.H - 1);
-        const uint8_t* row = in + (long long)y * a.in_pitch;
-        const int x = x0 - 4 + 4 * wc;
-        uint32_t w;
-        if (x >= 0 && x < a.W) w = __ldg(reinterpret_cast<const unsigned int*>(row + x));
-        else w = 0x01010101u * row[x < 0 ? 0 : a.W - 1];
-        *reinterpret_cast<uint32_t*>(in_s + r * T::IN_PITCH + 4 * wc) = w;
+    // 1. input rows y0-R .. y0+32+R, columns x0-4 .. x0+131, clamped (R32).  Smem column
+    //    j of row r holds image column xs + j, xs = (x0 - 4) rounded down to 16 bytes; the
+    //    tile starts at column o = x0 - 4 - xs (a multiple of 4).  Interior tiles (the 160
+    //    bytes of every row inside the image rows and the row pitch): asynchronous 16-byte
+    //    copies.  Border tiles: clamped 4-pixel words (W % 4 == 0, so a word is wholly inside
+    //    or wholly outside the image; an outside word repeats the nearest border pixel).
+    const int xs = (x0 - 4) & ~15, o = (x0 - 4) - xs;
+    const bool interior = (((uintptr_t)in | (uintptr_t)a.in_pitch) & 15) == 0 && xs >= 0 &&
+                          xs + T::IN_PITCH <= a.in_pitch && x0 + kPfTileX + R <= a.W && y0 - R >= 0 &&
+                          y0 - R + T::IN_H <= a.H;
+    if (interior) {
+        const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(in_s);
+        const uint8_t* src0 = in + (long long)(y0 - R) * a.in_pitch + xs;
+        for (int i = threadIdx.x; i < T::IN_H * (T::IN_PITCH / 16); i += kPfThreads) {
+            const int r = i / (T::IN_PITCH / 16), c = i - r * (T::IN_PITCH / 16);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + r * T::IN_PITCH + 16 * c),
+                         "l"(src0 + (long long)r * a.in_pitch + 16 * c) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    } else {
+        constexpr int WORDS = 34;
+        for (int i = threadIdx.x; i < T::IN_H * WORDS; i += kPfThreads) {
+            const int r = i / WORDS, wc = i - r * WORDS;
+            const int y = min(max(y0 - R + r, 0), a.H - 1);
+            const uint8_t* row = in + (long long)y * a.in_pitch;
+            const int x = x0 - 4 + 4 * wc;
+            uint32_t w;
+            if (x >= 0 && x < a.W) w = __ldg(reinterpret_cast<const unsigned int*>(row + x));
+            else w = 0x01010101u * row[x < 0 ? 0 : a.W - 1];
+            *reinterpret_cast<uint32_t*>(in_s + r * T::IN_PITCH + o + 4 * wc) = w;
+        }
     }
     __syncthreads();
 
@@ -135,7 +153,7 @@ __global__ void __launch_bounds__(kPfThreads) dmsgm_prefilter_kernel(const Prefi
             {
                 const int g = lane;
                 // inputs of v columns 4g .. 4g+3: smem columns 4g + (4 - R) + k, k = 0 .. 3 + 2G
-                const uint32_t* src = reinterpret_cast<const uint32_t*>(in_s + r * T::IN_PITCH + 4 * g);
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(in_s + r * T::IN_PITCH + o + 4 * g);
                 const uint32_t w0 = src[0], w1 = src[1], w2 = src[2];
                 float p[4 + 2 * G];
 #pragma unroll
@@ -176,7 +194,7 @@ __global__ void __launch_bounds__(kPfThreads) dmsgm_prefilter_kernel(const Prefi
     } else {
         // no Gaussian: v = the input (v column c <-> smem column c + 4 - M)
         for (int r = warp; r < T::V_H; r += kPfThreads / 32)
-            for (int c = lane; c < T::V_W; c += 32) v_s[r * T::V_PITCH + c] = in_s[r * T::IN_PITCH + c + 4 - M];
+            for (int c = lane; c < T::V_W; c += 32) v_s[r * T::V_PITCH + c] = in_s[r * T::IN_PITCH + o + c + 4 - M];
     }
     __syncthreads();
 
