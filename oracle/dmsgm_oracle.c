@@ -75,7 +75,7 @@ static int project_block(int Wb, int Hb, int N, const double* h, int bi, int bj,
     float Y = (float)(N * bj) + (float)N / 2.0f;
     float e = fmaf(g6, X, fmaf(g7, Y, g8));      /* w - 1 */
     float w = 1.0f + e;
-    if (!(w > 0.0f)) return 1;
+    if (!(w > 0x1p-100f && w < 0x1p100f)) return 1;   /* R5: w <= 0 or a degenerate projective scale */
     float px = fmaf(-X, e, fmaf(g0, X, fmaf(g1, Y, g2)));
     float py = fmaf(-Y, e, fmaf(g3, X, fmaf(g4, Y, g5)));
     float rw = 1.0f / w;

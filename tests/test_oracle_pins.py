@@ -396,6 +396,13 @@ def test_exposure(oracle_mod):
                 e, *_ = oracle_mod.mix_weights(W, Hh, N, H, bi, bj)
                 exposed_any |= e
         assert exposed_any
+    # R5: a projective scale outside (2^-100, 2^100) is degenerate: every block is exposed
+    for H in (np.array([1, 0, 0, 0, 1, 0, 0, 0, 1e31]),           # w = 1e31 everywhere
+              np.array([1, 0, 0, 0, 1, 0, 0, 0, 1e-31])):         # w = 1e-31 everywhere (px = 0 for no block)
+        for bi in range(W // N):
+            for bj in range(Hh // N):
+                e, *_ = oracle_mod.mix_weights(W, Hh, N, H, bi, bj)
+                assert e, (H, bi, bj)
 
 
 # --------------------------------------------------------------------------
