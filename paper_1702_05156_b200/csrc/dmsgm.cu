@@ -1087,7 +1087,7 @@ int dmsgm_band_halo_needed(int width, int height, int block, const double* H, in
                 const float X = (float)(N * bi) + 0.5f * (float)N;
                 const float e = fmaf(gg[6], X, r7);
                 const float w = 1.0f + e;
-                if (!(w > 0.0f)) continue;
+                if (!(w > 0x1p-100f && w < 0x1p100f)) continue;   // exposed (R5)
                 const float px = fmaf(-X, e, fmaf(gg[0], X, r1));
                 const float py = fmaf(-Y, e, fmaf(gg[3], X, r4));
                 const float rwN = (1.0f / w) * (1.0f / (float)N);

@@ -127,7 +127,7 @@ def test_random_state_parity(cuda_lib, oracle_mod, N, W, H, S, variant, kernel_p
 def test_exposure_parity(cuda_lib, oracle_mod, kernel_path):
     """Large motions, w <= 0 and far-out projections: exposed blocks reset identically."""
     rng = np.random.default_rng(5)
-    N, W, H, S = 4, 64, 32, 4
+    N, W, H, S = 4, 64, 32, 6
     pg, po = params_pair(cuda_lib, oracle_mod, S)
     init = np.stack([synth.random_state(rng, H // N, W // N) for _ in range(S)])
     frames = rng.integers(0, 256, (2, S, H, W)).astype(np.uint8)
@@ -136,6 +136,8 @@ def test_exposure_parity(cuda_lib, oracle_mod, kernel_path):
     Hs[:, 1] = [1, 0, 40, 0, 1, -20, 0, 0, 1]         # large shift: partly exposed
     Hs[:, 2] = [1, 0, 0, 0, 1, 0, 0.02, 0, -0.5]      # w changes sign inside the frame
     Hs[:, 3] = [1, 0, 1e7, 0, 1, 0, 0, 0, 1]          # far out
+    Hs[:, 4] = [1, 0, 0, 0, 1, 0, 1e31, 0, 1]         # w >= 2^100: degenerate scale (R5), sources near 0
+    Hs[:, 5] = [1, 0, 0, 0, 1, 0, 1e29, 0, 1]         # w crosses 2^100 inside the frame
     _check_run(cuda_lib, oracle_mod, frames, Hs, N, pg, po, init=init)
 
 
