@@ -247,7 +247,8 @@ KParams kparams(const dmsgm_params& p) {
 
 size_t plane_elems(const dmsgm_ctx* c) { return (size_t)c->Wb * (size_t)c->Hb; }
 int tiles_x_of(const dmsgm_ctx* c) { return (c->Wb + kTile - 1) / kTile; }
-// floats of one stream's state in the internal layout [Hb][4*tiles_x][6] (24-byte block records)
+// floats of one stream's state in the internal layout [Hb][4*tiles_x][6] (24-byte block records,
+// slots mu_A mu_C var_A var_C age_A age_C)
 size_t stream_floats(const dmsgm_ctx* c) { return (size_t)c->Hb * tiles_x_of(c) * kTileFloats; }
 
 // public [6][Hb][Wb] <-> internal [Hb][4*tiles_x][6] (host side, not on the hot path)
@@ -258,7 +259,7 @@ void to_public(const dmsgm_ctx* c, const float* in, float* out) {
         for (int by = 0; by < c->Hb; ++by)
             for (int bx = 0; bx < c->Wb; ++bx)
                 out[p * pe + (size_t)by * c->Wb + bx] =
-                    in[(size_t)by * tx * kTileFloats + (size_t)bx * kPlanes + p];
+                    in[(size_t)by * tx * kTileFloats + (size_t)bx * kPlanes + rec_slot(p)];
 }
 void to_internal(const dmsgm_ctx* c, const float* in, float* out) {
     const size_t pe = plane_elems(c);
@@ -267,7 +268,7 @@ void to_internal(const dmsgm_ctx* c, const float* in, float* out) {
     for (int p = 0; p < 6; ++p)
         for (int by = 0; by < c->Hb; ++by)
             for (int bx = 0; bx < c->Wb; ++bx)
-                out[(size_t)by * tx * kTileFloats + (size_t)bx * kPlanes + p] =
+                out[(size_t)by * tx * kTileFloats + (size_t)bx * kPlanes + rec_slot(p)] =
                     in[p * pe + (size_t)by * c->Wb + bx];
 }
 
