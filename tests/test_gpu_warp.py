@@ -112,3 +112,55 @@ def test_motion_mode_errors(cuda_lib, oracle_mod):
     x = torch.zeros((1, 8, 6), dtype=torch.uint8, device="cuda")                # width % 4 != 0
     with pytest.raises(cuda_lib.DmsgmError):
         cuda_lib.warp_frames(x, torch.zeros((1, 9), dtype=torch.float64, device="cuda"), x)
+
+
+def _translation(dx, dy):
+    return np.array([1, 0, dx, 0, 1, dy, 0, 0, 1], dtype=np.float64)
+
+
+def _similarity(W, H, zoom, rot_deg, dx=0.0, dy=0.0):
+    cx, cy = W / 2.0, H / 2.0
+    th = rot_deg * np.pi / 180.0
+    c, s = zoom * np.cos(th), zoom * np.sin(th)
+    A = np.array([[c, -s, cx + dx - c * cx + s * cy], [s, c, cy + dy - s * cx - c * cy], [0, 0, 1.0]])
+    return A.reshape(9)
+
+
+@pytest.mark.parametrize("case", ["shifts", "half_pixel", "far_out", "zoom_rot", "fallback", "unaligned_pitch"])
+def test_warp_fast_tiles(cuda_lib, oracle_mod, case):
+    """The fast-tile path (border-replicated box at a fixed pitch, magic-number floor and
+    byte conversion, paired arithmetic) and the fallbacks it hands over to, bit for bit
+    against the oracle: border tiles with samples far outside the frame, exact integer
+    and half-pixel positions (fx = 0, rounding ties), zoom/rotation/perspective at 1080p
+    width, maps whose source box exceeds the fixed pitch or row budget (clamped staged
+    box / global gathers), and a row pitch that is not a multiple of 16 (no fast tiles)."""
+    import torch
+    rng = np.random.default_rng(sum(map(ord, case)))
+    W, H = (1920, 72) if case in ("zoom_rot", "fallback") else (512, 80)
+    homs = {
+        "shifts": [_translation(3, -2), _translation(-7.25, 5.5), _translation(1.0 / 3, -40.7), _translation(37, 0.125)],
+        "half_pixel": [_translation(0.5, 0), _translation(-0.5, 0.5), _translation(2.5, -1.5), _translation(0, 0)],
+        "far_out": [_translation(-300, 3), _translation(5, 200), _translation(600, -600), _translation(-1.5, -70)],
+        "zoom_rot": [_similarity(W, H, 1.0005, 0.05, 1.3, -0.7), _similarity(W, H, 0.98, -2.0, -3, 2),
+                     synth.random_homography(rng, W, H, shift=4, rot_deg=3, zoom=0.05, persp=2e-5),
+                     _similarity(W, H, 1.2, 0.0)],
+        "fallback": [_similarity(W, H, 3.0, 0.0), _similarity(W, H, 1.0, 30.0), _similarity(W, H, 0.3, 5.0, 9, 9),
+                     np.array([1, 0, 0, 0, 1, 0, 2e-3, 0, 1.0])],
+        "unaligned_pitch": [_translation(3, -2), _similarity(W, H, 1.01, 1.0, 2, 2), _translation(-0.5, 20),
+                            _translation(0, 0)],
+    }[case]
+    Hs = np.stack(homs)
+    S = len(Hs)
+    yy, xx = np.mgrid[0:H, 0:W]
+    frames = np.clip(120 + 90 * np.sin(xx / 5.0 + yy / 7.0) + rng.normal(0, 20, (S, H, W)), 0, 255).astype(np.uint8)
+    dev = torch.device("cuda", 0)
+    pitch = W + 4 if case == "unaligned_pitch" else W
+    fin = torch.zeros((S, H, pitch), dtype=torch.uint8, device=dev)
+    fin[..., :W] = torch.from_numpy(frames).to(dev)
+    fout = torch.full((S, H, pitch), 7, dtype=torch.uint8, device=dev)
+    cuda_lib.warp_frames(fin[..., :W], torch.from_numpy(Hs).to(dev), fout[..., :W])
+    torch.cuda.synchronize()
+    got = fout[..., :W].cpu().numpy()
+    want = oracle_mod.warp_frames(frames, Hs)
+    for s in range(S):
+        assert np.array_equal(got[s], want[s]), f"{case} stream {s}: {(got[s] != want[s]).sum()} pixels differ"
