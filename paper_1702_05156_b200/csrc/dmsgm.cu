@@ -301,10 +301,20 @@ cudaError_t launch_warp(int W, int H, int count, const uint8_t* in, long long in
     WarpArgs a;
     a.in = in; a.in_stride = in_stride; a.in_pitch = (int)in_pitch;
     a.out = out; a.out_stride = out_stride; a.out_pitch = (int)out_pitch;
-    a.H = Hs; a.W = W; a.Hh = H;
-    const dim3 block(kWarpThreadsX, kWarpRows, 1);
-    const dim3 grid((W / 4 + kWarpThreadsX - 1) / kWarpThreadsX, (H + kWarpTileY - 1) / kWarpTileY, count);
-    dmsgm_warp_kernel<<<grid, block, 0, stream>>>(a);
+    a.H = Hs; a.W = W; a.Hh = H; a.count = count;
+    // persistent: up to 4 CTAs per SM (registers and the two 24 KB source-box stages)
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+        cudaFuncSetAttribute(dmsgm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpDynSmem);
+    }
+    const long long tiles = (long long)((W / 4 + kWarpThreadsX - 1) / kWarpThreadsX) *
+                            ((H + kWarpTileY - 1) / kWarpTileY) * count;
+    const int grid = (int)(tiles < 4LL * sms ? tiles : 4LL * sms);
+    if (grid == 0) return cudaSuccess;
+    dmsgm_warp_kernel<<<grid, kWarpThreads, kWarpDynSmem, stream>>>(a);
     return cudaGetLastError();
 }
 
