@@ -303,12 +303,17 @@ cudaError_t launch_warp(int W, int H, int count, const uint8_t* in, long long in
     a.out = out; a.out_stride = out_stride; a.out_pitch = (int)out_pitch;
     a.H = Hs; a.W = W; a.Hh = H; a.count = count;
     // persistent: up to 4 CTAs per SM (registers and the two 24 KB source-box stages)
-    static int sms = 0;
+    // (per device: the dynamic shared-memory opt-in is a per-device function attribute)
+    static int sms_of[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& sms = sms_of[dev & 63];
     if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-        cudaFuncSetAttribute(dmsgm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpDynSmem);
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        cudaError_t e = cudaFuncSetAttribute(dmsgm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpDynSmem);
+        if (e != cudaSuccess) return e;
+        sms = n;
     }
     const long long tiles = (long long)((W / 4 + kWarpThreadsX - 1) / kWarpThreadsX) *
                             ((H + kWarpTileY - 1) / kWarpTileY) * count;

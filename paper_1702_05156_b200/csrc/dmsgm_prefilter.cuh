@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include "dmsgm_math.cuh"
+#include "dmsgm_pair.cuh"
 
 namespace dmsgm {
 
@@ -99,6 +100,12 @@ __device__ __forceinline__ uint32_t byte_at(uint32_t w0, uint32_t w1, uint32_t w
     return (w >> (8 * (k & 3))) & 0xFFu;
 }
 
+// 0x4B000000 | byte k of the 12-byte string w0 w1 w2 (k a compile-time constant): one PRMT
+__device__ __forceinline__ uint32_t byte_magic(uint32_t w0, uint32_t w1, uint32_t w2, int k) {
+    const uint32_t w = k < 4 ? w0 : (k < 8 ? w1 : w2);
+    return __byte_perm(w, 0x4B000000u, 0x7540u | (uint32_t)(k & 3));
+}
+
 template <int G, int M>
 __global__ void __launch_bounds__(kPfThreads) dmsgm_prefilter_kernel(const PrefilterArgs a) {
     using T = PfTile<G, M>;
@@ -155,18 +162,26 @@ __global__ void __launch_bounds__(kPfThreads) dmsgm_prefilter_kernel(const Prefi
                 // inputs of v columns 4g .. 4g+3: smem columns 4g + (4 - R) + k, k = 0 .. 3 + 2G
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(in_s + r * T::IN_PITCH + o + 4 * g);
                 const uint32_t w0 = src[0], w1 = src[1], w2 = src[2];
-                float p[4 + 2 * G];
+                // bytes as exact floats without conversion instructions: (0x4B000000 | b) is
+                // 2^23 + b, minus 2^23 (pairs of FADD2)
+                float p[4 + 2 * G + 1];
 #pragma unroll
-                for (int k = 0; k < 4 + 2 * G; ++k) p[k] = (float)byte_at(w0, w1, w2, k + 4 - R);
-                float o[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    float blur = 0.0f;
-#pragma unroll
-                    for (int t = 0; t <= 2 * G; ++t) blur = f_fma(p[q + t], a.taps[t], blur);
-                    o[q] = blur;
+                for (int k = 0; k < 4 + 2 * G; k += 2) {
+                    const float2 m = make_float2(__uint_as_float(byte_magic(w0, w1, w2, k + 4 - R)),
+                                                 __uint_as_float(byte_magic(w0, w1, w2, k + 5 - R)));
+                    const float2 v = f2_sub(m, f2_bc(8388608.0f));
+                    p[k] = v.x;
+                    p[k + 1] = v.y;
                 }
-                *reinterpret_cast<float4*>(h_s + r * T::H_PITCH + 4 * g) = make_float4(o[0], o[1], o[2], o[3]);
+                // outputs (0, 1) and (2, 3) as pairs: blur_q = fma(p[q + t], tap_t, blur_q),
+                // t ascending from 0 (R31), lane by lane
+                float2 o01 = f2_bc(0.0f), o23 = f2_bc(0.0f);
+#pragma unroll
+                for (int t = 0; t <= 2 * G; ++t) {
+                    o01 = f2_fma(make_float2(p[t], p[t + 1]), f2_bc(a.taps[t]), o01);
+                    o23 = f2_fma(make_float2(p[t + 2], p[t + 3]), f2_bc(a.taps[t]), o23);
+                }
+                *reinterpret_cast<float4*>(h_s + r * T::H_PITCH + 4 * g) = make_float4(o01.x, o01.y, o23.x, o23.y);
             }
         }
         __syncthreads();
@@ -175,19 +190,18 @@ __global__ void __launch_bounds__(kPfThreads) dmsgm_prefilter_kernel(const Prefi
         for (int r = warp; r < T::V_H; r += kPfThreads / 32) {
             {
                 const int g = lane;
-                float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                float2 acc01 = f2_bc(0.0f), acc23 = f2_bc(0.0f);
 #pragma unroll
                 for (int t = 0; t <= 2 * G; ++t) {
                     const float4 h = *reinterpret_cast<const float4*>(h_s + (r + t) * T::H_PITCH + 4 * g);
-                    acc[0] = f_fma(h.x, a.taps[t], acc[0]);
-                    acc[1] = f_fma(h.y, a.taps[t], acc[1]);
-                    acc[2] = f_fma(h.z, a.taps[t], acc[2]);
-                    acc[3] = f_fma(h.w, a.taps[t], acc[3]);
+                    acc01 = f2_fma(make_float2(h.x, h.y), f2_bc(a.taps[t]), acc01);
+                    acc23 = f2_fma(make_float2(h.z, h.w), f2_bc(a.taps[t]), acc23);
                 }
-                uint32_t u[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) u[q] = __float2uint_rn(acc[q]);      // nearest, ties to even
-                const uint32_t w = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
+                // nearest, ties to even: acc in [0, 255.5), so acc + 2^23 rounds to 2^23 + rint(acc)
+                // and its low byte is the result
+                const float2 u01 = f2_add(acc01, f2_bc(8388608.0f)), u23 = f2_add(acc23, f2_bc(8388608.0f));
+                const uint32_t w = __byte_perm(__byte_perm(__float_as_uint(u01.x), __float_as_uint(u01.y), 0x0040),
+                                               __byte_perm(__float_as_uint(u23.x), __float_as_uint(u23.y), 0x0040), 0x5410);
                 *reinterpret_cast<uint32_t*>(v_s + r * T::V_PITCH + 4 * g) = w;
             }
         }
