@@ -163,8 +163,8 @@ void dmsgm_destroy(dmsgm_ctx* ctx);
 int dmsgm_set_prefilter(dmsgm_ctx* ctx, int gauss_size, float gauss_sigma, int median_radius);
 
 /* Stand-alone filter of `count` frames: in u8 [count][height][in_pitch], out u8
- * [count][height][out_pitch] (device; width % 4 == 0, out 4-byte aligned, out_pitch % 4
- * == 0).  Enqueued on cuda_stream; DMSGM_EINVAL for bad arguments. */
+ * [count][height][out_pitch] (device; width % 4 == 0; in, out 4-byte aligned, in_pitch % 4
+ * == 0, out_pitch % 4 == 0).  Enqueued on cuda_stream; DMSGM_EINVAL for bad arguments. */
 int dmsgm_prefilter(int width, int height, int count, const uint8_t* in, size_t in_pitch, uint8_t* out,
                     size_t out_pitch, int gauss_size, float gauss_sigma, int median_radius, void* cuda_stream);
 

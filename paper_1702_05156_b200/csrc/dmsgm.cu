@@ -331,8 +331,9 @@ cudaError_t launch_prefilter(int W, int H, int count, const uint8_t* in, long lo
     a.out = out; a.out_stride = out_stride; a.out_pitch = (int)out_pitch;
     a.W = W; a.H = H; a.g = g; a.m = m;
     for (int i = 0; i < 2 * kPfMaxG + 1; ++i) a.taps[i] = i < 2 * g + 1 ? taps[i] : 0.0f;
-    const dim3 grid((W + kPfTileX - 1) / kPfTileX, (H + kPfTileY - 1) / kPfTileY, count);
-#define DMSGM_PF(GG, MM) dmsgm_prefilter_kernel<GG, MM><<<grid, kPfThreads, 0, stream>>>(a)
+    const int strips = (W + kPfOutW - 1) / kPfOutW;
+    const dim3 grid((strips + kPfWarps - 1) / kPfWarps, (H + kPfBand - 1) / kPfBand, count);
+#define DMSGM_PF(GG, MM) dmsgm_prefilter_kernel<GG, MM><<<grid, 32 * kPfWarps, 0, stream>>>(a)
     switch (g * 2 + m) {
         case 0: DMSGM_PF(0, 0); break;
         case 1: DMSGM_PF(0, 1); break;
@@ -837,7 +838,7 @@ int dmsgm_prefilter(int width, int height, int count, const uint8_t* in, size_t 
                     size_t out_pitch, int gauss_size, float gauss_sigma, int median_radius, void* stream) {
     float taps[2 * kPfMaxG + 1];
     if (!in || !out || width < 4 || width % 4 || height < 1 || count < 1 || in_pitch < (size_t)width ||
-        out_pitch < (size_t)width || (out_pitch & 3) || ((uintptr_t)out & 3))
+        out_pitch < (size_t)width || (out_pitch & 3) || ((uintptr_t)out & 3) || (in_pitch & 3) || ((uintptr_t)in & 3))
         return DMSGM_EINVAL;
     if (median_radius < 0 || median_radius > 1 || !gauss_taps(gauss_size, gauss_sigma, taps)) return DMSGM_EINVAL;
     cudaError_t e = launch_prefilter(width, height, count, in, (long long)height * in_pitch, in_pitch, out,

@@ -2,17 +2,11 @@
 // separable Gaussian then 3x3 median (§2.1, §3.3.1, App. A/B;
 // readings R30-R34 of DESIGN.md §2).
 //
-// One kernel, one 124 x 32 output tile per CTA (256 threads), everything in shared memory:
-//   1. the input tile with a halo of R = g + m pixels (g = Gaussian radius, m = median
-//      radius) is loaded with CLAMPED coordinates (R32) -- which makes both Gaussian
-//      passes exact without further clamping (a row pass depends only on its image row);
-//   2. row pass (fp32, fma chain in ascending tap order, R31) -> float tile;
-//   3. column pass -> rounded to nearest-even, clamped to [0, 255] -> u8 tile;
-//      positions outside the image are then overwritten by their clamped source (the
-//      median's border rule, R32, R33);
-//   4. 3x3 median of 4 pixels per thread (sorted columns, native u16x2 min/max),
-//      written as 32-bit words.
-// HBM traffic: 1 B/px read + 1 B/px written; the step kernel then reads the output.
+// One streaming kernel (see dmsgm_prefilter_kernel below): a warp walks a 120-column strip
+// of a frame down kPfBand rows, with the row pass, the column pass (a register ring of
+// partial sums) and the median in registers -- no shared memory, no CTA barriers.
+// HBM traffic: 1 B/px read (+ the strips' 1-column and band halos, L2) + 1 B/px written;
+// the step kernel then reads the output.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,9 +16,6 @@
 
 namespace dmsgm {
 
-constexpr int kPfTileX = 124;     // output columns per CTA (+ the median halo = 32 groups of 4)
-constexpr int kPfTileY = 32;      // output rows per CTA
-constexpr int kPfThreads = 256;
 constexpr int kPfMaxG = 3;        // Gaussian radius <= 3 (size <= 7)
 
 struct PrefilterArgs {
@@ -62,8 +53,10 @@ __device__ __forceinline__ uint32_t median3x3x4(const uint32_t (&w0)[3], const u
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             lo[k][0] = __vimin3_u16x2(c[k][0], c[k][1], c[k][2]);
-            mi[k][0] = med3_u16x2(c[k][0], c[k][1], c[k][2]);
             hi[k][0] = __vimax3_u16x2(c[k][0], c[k][1], c[k][2]);
+            // the middle one is the sum minus the extremes (lanes <= 3 * 255: no carry or
+            // borrow crosses the 16-bit lanes)
+            mi[k][0] = c[k][0] + c[k][1] + c[k][2] - lo[k][0] - hi[k][0];
         }
     }
     // windows of outputs (x, x+1): column pairs (x-1,x) (x,x+1) (x+1,x+2);
@@ -78,182 +71,151 @@ __device__ __forceinline__ uint32_t median3x3x4(const uint32_t (&w0)[3], const u
     return __byte_perm(p01, p23, 0x6420);      // (x, x+1, x+2, x+3) as bytes
 }
 
-// G = Gaussian radius, M = median radius (compile-time: the tile geometry depends on them)
-template <int G, int M>
-struct PfTile {
-    static constexpr int R = G + M;                       // input halo (<= 4)
-    static constexpr int IN_H = kPfTileY + 2 * R;         // input tile rows
-    // input tile columns: x0 - 4 .. x0 + 128 + 4 (+ slack), so the tile's first column x0
-    // sits on a 4-byte boundary: smem column j <-> image column x0 - 4 + j
-    static constexpr int IN_PITCH = 160;                  // 10 chunks of 16 bytes (see the load)
-    static constexpr int V_W = kPfTileX + 2 * M;          // Gaussian output columns (median halo)
-    static constexpr int V_H = kPfTileY + 2 * M;
-    static constexpr int H_PITCH = 128;                   // floats per row-pass row: 32 groups of 4
-                                                          // (one per lane; V_W <= 126 are used)
-    static constexpr int V_PITCH = 144;                   // bytes per Gaussian-output row
-    static_assert(R <= 4, "halo of at most 4 pixels");
-};
-
-__device__ __forceinline__ uint32_t byte_at(uint32_t w0, uint32_t w1, uint32_t w2, int k) {
-    // byte k (0..11) of the 12-byte little-endian string w0 w1 w2 (k is a compile-time constant)
-    const uint32_t w = k < 4 ? w0 : (k < 8 ? w1 : w2);
-    return (w >> (8 * (k & 3))) & 0xFFu;
-}
-
 // 0x4B000000 | byte k of the 12-byte string w0 w1 w2 (k a compile-time constant): one PRMT
 __device__ __forceinline__ uint32_t byte_magic(uint32_t w0, uint32_t w1, uint32_t w2, int k) {
     const uint32_t w = k < 4 ? w0 : (k < 8 ? w1 : w2);
     return __byte_perm(w, 0x4B000000u, 0x7540u | (uint32_t)(k & 3));
 }
 
+// ---------------------------------------------------------------------------
+// Streaming kernel: no shared memory, no CTA barriers.  A warp owns a vertical strip of
+// 120 output columns x kPfBand rows of one frame; lane L holds the 4 columns
+// gx = xw - 4 + 4L .. gx + 3 (lanes 0 and 31 are the strip's 1-column halo; lanes 1-30
+// produce output) and walks down the strip:
+//   input row r (clamped, R32): one 32-bit load per lane, prefetched kPfRing rows ahead;
+//     the neighbours' words by two shuffles give bytes gx-4 .. gx+7;
+//   row pass (R31): 4 outputs as 2 pairs ((0, 2), (1, 3)), fma(p, tap_t, acc) ascending
+//     t, bytes made exact floats by a PRMT into 0x4B000000 and one paired subtraction;
+//   column pass: input row r contributes tap t to Gaussian row r + G - t, so 2G+1
+//     partial accumulators rotate through a register ring (the row loop is unrolled by
+//     the ring size, so every ring index is a compile-time constant); row r - G is
+//     complete at tap 2G: rounded to nearest-even (acc + 2^23, low byte);
+//   median (R33): the last 3 Gaussian rows as (x-1 .. x+2, x+3 .. x+6) word pairs (two
+//     shuffles + PRMT per Gaussian row), median3x3x4, one 32-bit store.
+// Borders: input rows / columns are clamped (the passes stay exact); Gaussian values
+// outside the image take their clamped value for the median (R32): Gaussian row -1 / H
+// is row 0 / H-1 again, column -1 / W is column 0 / W-1 again.
+// ---------------------------------------------------------------------------
+constexpr int kPfOutW = 120;      // output columns per warp (lanes 1..30)
+#ifndef DMSGM_PF_BAND
+#define DMSGM_PF_BAND 40
+#endif
+constexpr int kPfBand = DMSGM_PF_BAND;   // output rows per warp (A/B at C4: 32/40/48/64 rows -> 117.6/115.1/119.0/121.2 us)
+constexpr int kPfWarps = 8;       // warps per CTA (independent strips)
+
 template <int G, int M>
-__global__ void __launch_bounds__(kPfThreads) dmsgm_prefilter_kernel(const PrefilterArgs a) {
-    using T = PfTile<G, M>;
-    constexpr int R = T::R;
-    __shared__ __align__(16) uint8_t in_s[T::IN_H * T::IN_PITCH];
-    __shared__ __align__(16) float h_s[G > 0 ? T::IN_H * T::H_PITCH : 4];
-    __shared__ __align__(16) uint8_t v_s[T::V_H * T::V_PITCH];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int x0 = blockIdx.x * kPfTileX, y0 = blockIdx.y * kPfTileY, s = blockIdx.z;
+__global__ void __launch_bounds__(32 * kPfWarps) dmsgm_prefilter_kernel(const PrefilterArgs a) {
+    constexpr int NR = 2 * G + 1;                   // column-pass ring (rows in flight)
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * kPfWarps + (threadIdx.x >> 5);
+    const int xw = strip * kPfOutW;
+    if (xw >= a.W) return;                          // warp-uniform
+    const int s = blockIdx.z;
+    const int ys = blockIdx.y * kPfBand;
+    const int ye = min(ys + kPfBand, a.H);          // output rows [ys, ye)
     const uint8_t* in = a.in + (long long)s * a.in_stride;
-
-    // 1. input rows y0-R .. y0+32+R, columns x0-4 .. x0+131, clamped (R32).  Smem column
-    //    j of row r holds image column xs + j, xs = (x0 - 4) rounded down to 16 bytes; the
-    //    tile starts at column o = x0 - 4 - xs (a multiple of 4).  Interior tiles (the 160
-    //    bytes of every row inside the image rows and the row pitch): asynchronous 16-byte
-    //    copies.  Border tiles: clamped 4-pixel words (W % 4 == 0, so a word is wholly inside
-    //    or wholly outside the image; an outside word repeats the nearest border pixel).
-    const int xs = (x0 - 4) & ~15, o = (x0 - 4) - xs;
-    const bool interior = (((uintptr_t)in | (uintptr_t)a.in_pitch) & 15) == 0 && xs >= 0 &&
-                          xs + T::IN_PITCH <= a.in_pitch && x0 + kPfTileX + R <= a.W && y0 - R >= 0 &&
-                          y0 - R + T::IN_H <= a.H;
-    if (interior) {
-        const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(in_s);
-        const uint8_t* src0 = in + (long long)(y0 - R) * a.in_pitch + xs;
-        for (int i = threadIdx.x; i < T::IN_H * (T::IN_PITCH / 16); i += kPfThreads) {
-            const int r = i / (T::IN_PITCH / 16), c = i - r * (T::IN_PITCH / 16);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + r * T::IN_PITCH + 16 * c),
-                         "l"(src0 + (long long)r * a.in_pitch + 16 * c) : "memory");
-        }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-    } else {
-        constexpr int WORDS = 34;
-        for (int i = threadIdx.x; i < T::IN_H * WORDS; i += kPfThreads) {
-            const int r = i / WORDS, wc = i - r * WORDS;
-            const int y = min(max(y0 - R + r, 0), a.H - 1);
-            const uint8_t* row = in + (long long)y * a.in_pitch;
-            const int x = x0 - 4 + 4 * wc;
-            uint32_t w;
-            if (x >= 0 && x < a.W) w = __ldg(reinterpret_cast<const unsigned int*>(row + x));
-            else w = 0x01010101u * row[x < 0 ? 0 : a.W - 1];
-            *reinterpret_cast<uint32_t*>(in_s + r * T::IN_PITCH + o + 4 * wc) = w;
-        }
-    }
-    __syncthreads();
-
-    // Gaussian output v_s: image rows y0-M .. y0+32+M, columns x0-M .. x0+128+M
-    // (v column c <-> image column x0 - M + c)
-    if constexpr (G > 0) {
-        // 2. row pass, fp32 fma chain in ascending tap order (R31): every input row, 32
-        //    groups of 4 output columns (lane l: group l)
-        for (int r = warp; r < T::IN_H; r += kPfThreads / 32) {
-            {
-                const int g = lane;
-                // inputs of v columns 4g .. 4g+3: smem columns 4g + (4 - R) + k, k = 0 .. 3 + 2G
-                const uint32_t* src = reinterpret_cast<const uint32_t*>(in_s + r * T::IN_PITCH + o + 4 * g);
-                const uint32_t w0 = src[0], w1 = src[1], w2 = src[2];
-                // bytes as exact floats without conversion instructions: (0x4B000000 | b) is
-                // 2^23 + b, minus 2^23 (pairs of FADD2)
-                float p[4 + 2 * G + 1];
-#pragma unroll
-                for (int k = 0; k < 4 + 2 * G; k += 2) {
-                    const float2 m = make_float2(__uint_as_float(byte_magic(w0, w1, w2, k + 4 - R)),
-                                                 __uint_as_float(byte_magic(w0, w1, w2, k + 5 - R)));
-                    const float2 v = f2_sub(m, f2_bc(8388608.0f));
-                    p[k] = v.x;
-                    p[k + 1] = v.y;
-                }
-                // outputs (0, 1) and (2, 3) as pairs: blur_q = fma(p[q + t], tap_t, blur_q),
-                // t ascending from 0 (R31), lane by lane
-                float2 o01 = f2_bc(0.0f), o23 = f2_bc(0.0f);
-#pragma unroll
-                for (int t = 0; t <= 2 * G; ++t) {
-                    o01 = f2_fma(make_float2(p[t], p[t + 1]), f2_bc(a.taps[t]), o01);
-                    o23 = f2_fma(make_float2(p[t + 2], p[t + 3]), f2_bc(a.taps[t]), o23);
-                }
-                *reinterpret_cast<float4*>(h_s + r * T::H_PITCH + 4 * g) = make_float4(o01.x, o01.y, o23.x, o23.y);
-            }
-        }
-        __syncthreads();
-        // 3. column pass at the V_H rows, rounded once to u8 (R31).  No clamp is needed:
-        //    the taps are positive and sum to 1 within 1e-6, so 0 <= acc < 255.5
-        for (int r = warp; r < T::V_H; r += kPfThreads / 32) {
-            {
-                const int g = lane;
-                float2 acc01 = f2_bc(0.0f), acc23 = f2_bc(0.0f);
-#pragma unroll
-                for (int t = 0; t <= 2 * G; ++t) {
-                    const float4 h = *reinterpret_cast<const float4*>(h_s + (r + t) * T::H_PITCH + 4 * g);
-                    acc01 = f2_fma(make_float2(h.x, h.y), f2_bc(a.taps[t]), acc01);
-                    acc23 = f2_fma(make_float2(h.z, h.w), f2_bc(a.taps[t]), acc23);
-                }
-                // nearest, ties to even: acc in [0, 255.5), so acc + 2^23 rounds to 2^23 + rint(acc)
-                // and its low byte is the result
-                const float2 u01 = f2_add(acc01, f2_bc(8388608.0f)), u23 = f2_add(acc23, f2_bc(8388608.0f));
-                const uint32_t w = __byte_perm(__byte_perm(__float_as_uint(u01.x), __float_as_uint(u01.y), 0x0040),
-                                               __byte_perm(__float_as_uint(u23.x), __float_as_uint(u23.y), 0x0040), 0x5410);
-                *reinterpret_cast<uint32_t*>(v_s + r * T::V_PITCH + 4 * g) = w;
-            }
-        }
-    } else {
-        // no Gaussian: v = the input (v column c <-> smem column c + 4 - M)
-        for (int r = warp; r < T::V_H; r += kPfThreads / 32)
-            for (int c = lane; c < T::V_W; c += 32) v_s[r * T::V_PITCH + c] = in_s[r * T::IN_PITCH + o + c + 4 - M];
-    }
-    __syncthreads();
-
-    if constexpr (M > 0) {
-        // positions of v outside the image take their clamped value (the median clamps,
-        // R32); the sources are inside the image and never written here: no race
-        // (M = 1: at most the first / last row and the first / last columns of v; rows
-        // first, then columns, so a corner takes the clamped corner value)
-        const int last_r = min(T::V_H - 1, a.H - 1 - (y0 - M)), last_c = min(T::V_W - 1, a.W - 1 - (x0 - M));
-        if (y0 == 0 || last_r < T::V_H - 1) {
-            for (int c = threadIdx.x; c < T::V_W; c += kPfThreads) {
-                if (y0 == 0) v_s[c] = v_s[T::V_PITCH + c];
-                for (int r = last_r + 1; r < T::V_H; ++r) v_s[r * T::V_PITCH + c] = v_s[last_r * T::V_PITCH + c];
-            }
-            __syncthreads();
-        }
-        if (x0 == 0 || last_c < T::V_W - 1) {
-            for (int r = threadIdx.x; r < T::V_H; r += kPfThreads) {
-                uint8_t* row = v_s + r * T::V_PITCH;
-                if (x0 == 0) row[0] = row[1];
-                for (int c = last_c + 1; c < T::V_W; ++c) row[c] = row[last_c];
-            }
-            __syncthreads();
-        }
-    }
-
-    // 4. median (or the Gaussian output itself): a warp per output row, 4 pixels per lane
     uint8_t* out = a.out + (long long)s * a.out_stride;
-    for (int r = warp; r < kPfTileY; r += kPfThreads / 32) {
-        const int y = y0 + r, x = x0 + 4 * lane;
-        if (lane >= kPfTileX / 4 || y >= a.H || x >= a.W) continue;
-        uint32_t w;
-        if constexpr (M > 0) {
-            uint32_t w0[3], w1[3];
-#pragma unroll
-            for (int dy = 0; dy < 3; ++dy) {
-                const uint8_t* row = v_s + (r + dy) * T::V_PITCH + 4 * lane;
-                w0[dy] = *reinterpret_cast<const uint32_t*>(row);       // columns x-1 .. x+2
-                w1[dy] = *reinterpret_cast<const uint32_t*>(row + 4);   // x+3 .. x+6
-            }
-            w = median3x3x4(w0, w1);
+    const int gx = xw - 4 + 4 * lane;               // this lane's 4 columns
+    const int x = gx;                               // output columns (lanes 1..30)
+    const bool writer = lane >= 1 && lane <= 30 && x < a.W;
+    // Gaussian rows [g0, g1] feed the output rows (clamped to the image)
+    const int g0 = M ? max(ys - 1, 0) : ys, g1 = M ? min(ye, a.H - 1) : ye - 1;
+
+    auto load_word = [&](int r) -> uint32_t {       // clamped row r, columns gx .. gx+3 (clamped)
+        const uint8_t* row = in + (long long)min(max(r, 0), a.H - 1) * a.in_pitch;
+        if (gx >= 0 && gx + 4 <= a.W) return __ldg(reinterpret_cast<const unsigned int*>(row + gx));
+        return 0x01010101u * (uint32_t)__ldg(row + (gx < 0 ? 0 : a.W - 1));
+    };
+    // median window: (x-1 .. x+2, x+3 .. x+6) of the last 3 Gaussian rows.  The rows pushed
+    // are E(ys-1), E(ys), ..., E(ye) with E(y) = Gaussian row clamp(y) (R32): row 0 is pushed
+    // twice at the top of the image, row H-1 twice at the bottom; after push i >= 2 the
+    // window is centred on output row ys + i - 2.
+    uint32_t mw0[3] = {0, 0, 0}, mw1[3] = {0, 0, 0};
+    int pushed = 0;
+    auto emit_gauss = [&](int gy, uint32_t gw) {    // Gaussian row gy (bytes of columns gx .. gx+3)
+        if constexpr (M == 0) {
+            if (writer) *reinterpret_cast<uint32_t*>(out + (long long)gy * a.out_pitch + x) = gw;
         } else {
-            w = *reinterpret_cast<const uint32_t*>(v_s + r * T::V_PITCH + 4 * lane);
+            const uint32_t left = __shfl_up_sync(0xffffffffu, gw, 1), right = __shfl_down_sync(0xffffffffu, gw, 1);
+            uint32_t w0 = __byte_perm(left, gw, 0x6543), w1 = __byte_perm(gw, right, 0x6543);
+            if (x == 0) w0 = __byte_perm(w0, 0u, 0x3211);          // column -1 := column 0
+            if (x + 4 == a.W) w1 = __byte_perm(w1, 0u, 0x3200);    // column W := column W-1
+            const int reps = (gy == 0 ? 2 : 1) + (gy == a.H - 1 && ye == a.H ? 1 : 0);
+            for (int k = 0; k < reps; ++k) {
+                mw0[0] = mw0[1]; mw0[1] = mw0[2]; mw0[2] = w0;
+                mw1[0] = mw1[1]; mw1[1] = mw1[2]; mw1[2] = w1;
+                if (++pushed >= 3) {
+                    const int y = ys + pushed - 3;
+                    const uint32_t m = median3x3x4(mw0, mw1);
+                    if (writer) *reinterpret_cast<uint32_t*>(out + (long long)y * a.out_pitch + x) = m;
+                }
+            }
         }
-        *reinterpret_cast<uint32_t*>(out + (long long)y * a.out_pitch + x) = w;
+    };
+
+    if constexpr (G == 0) {
+        for (int gy = g0; gy <= g1; ++gy) emit_gauss(gy, load_word(gy));
+    } else {
+        float2 acc[NR][2];
+        uint32_t q[NR];                              // prefetched input words (ring, NR rows ahead)
+        const int r0 = g0 - G, r1 = g1 + G;          // input rows in streaming order
+#pragma unroll
+        for (int j = 0; j < NR; ++j) q[j] = load_word(r0 + j);
+#pragma unroll
+        for (int j = 0; j < NR; ++j) acc[j][0] = acc[j][1] = f2_bc(0.0f);
+        float tap[NR];
+#pragma unroll
+        for (int t = 0; t < NR; ++t) tap[t] = a.taps[t];
+        for (int rb = r0; rb <= r1; rb += NR) {
+#pragma unroll
+            for (int ph = 0; ph < NR; ++ph) {
+                const int r = rb + ph;
+                if (r > r1) break;                   // warp-uniform
+                const uint32_t w = q[ph];
+                q[ph] = load_word(r + NR);
+                // row pass of input row r
+                const uint32_t wl = __shfl_up_sync(0xffffffffu, w, 1), wr = __shfl_down_sync(0xffffffffu, w, 1);
+                // outputs paired (0, 2) and (1, 3): the operand pairs (p[k], p[k+2]),
+                // k = 0 .. 2G+1, are built directly by PRMT (no register moves)
+                float2 pp[2 * G + 2];
+#pragma unroll
+                for (int k = 0; k < 2 * G + 2; ++k)
+                    pp[k] = f2_sub(make_float2(__uint_as_float(byte_magic(wl, w, wr, k + 4 - G)),
+                                               __uint_as_float(byte_magic(wl, w, wr, k + 6 - G))),
+                                   f2_bc(8388608.0f));
+                float2 h01 = f2_bc(0.0f), h23 = f2_bc(0.0f);     // (h0, h2), (h1, h3)
+#pragma unroll
+                for (int t = 0; t < NR; ++t) {
+                    h01 = f2_fma(pp[t], f2_bc(tap[t]), h01);
+                    h23 = f2_fma(pp[t + 1], f2_bc(tap[t]), h23);
+                }
+                // column pass: row r is tap t of Gaussian row r + G - t, whose accumulator
+                // sits in ring slot (ph + G - t) mod NR (rb is a multiple of NR from r0)
+#pragma unroll
+                for (int t = 0; t < NR; ++t) {
+                    const int slot = (ph + G - t + 2 * NR) % NR;
+                    if (t == 0) {
+                        acc[slot][0] = f2_fma(h01, f2_bc(tap[0]), f2_bc(0.0f));
+                        acc[slot][1] = f2_fma(h23, f2_bc(tap[0]), f2_bc(0.0f));
+                    } else {
+                        acc[slot][0] = f2_fma(h01, f2_bc(tap[t]), acc[slot][0]);
+                        acc[slot][1] = f2_fma(h23, f2_bc(tap[t]), acc[slot][1]);
+                    }
+                }
+                // Gaussian row r - G is complete (tap 2G just added): round and emit
+                const int gy = r - G;
+                if (gy >= g0) {
+                    const int slot = (ph + G - 2 * G + 2 * NR) % NR;
+                    const float2 u01 = f2_add(acc[slot][0], f2_bc(8388608.0f));
+                    const float2 u23 = f2_add(acc[slot][1], f2_bc(8388608.0f));
+                    // u01 = (g0, g2), u23 = (g1, g3)
+                    const uint32_t gw = __byte_perm(__byte_perm(__float_as_uint(u01.x), __float_as_uint(u23.x), 0x0040),
+                                                    __byte_perm(__float_as_uint(u01.y), __float_as_uint(u23.y), 0x0040),
+                                                    0x5410);
+                    emit_gauss(gy, gw);
+                }
+            }
+        }
     }
 }
 
