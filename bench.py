@@ -453,11 +453,15 @@ def run_dmsgm(args, rank, world, local):
             "gpu_launches": info.kernels_per_step * args.steps,
             "clocks": clocks,
         }
-        if pf_roof:
-            # the dominant kernel of this step is the (ALU-bound) filter; the HBM figure of
-            # the whole step is kept as roofline_step
+        # with preprocessing and/or frame warping the dominant kernel of the step is the
+        # (ALU-bound) filter or warp kernel: it becomes `roofline`; the HBM figure of the
+        # whole step is kept as roofline_step
+        extra = [r for r in (pf_roof, warp_roof) if r]
+        if extra:
             line["roofline_step"] = line["roofline"]
-            line["roofline"] = pf_roof
+            line["roofline"] = max(extra, key=lambda r: r["share_of_step"])
+        if pf_roof:
+            line["roofline_prefilter"] = pf_roof
         if warp_roof:
             line["roofline_warp"] = warp_roof
         print(json.dumps(line), flush=True)

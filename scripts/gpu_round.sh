@@ -13,3 +13,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:dmsg
   -o $OUT/prof_${TAG}c5 -f python bench.py --config C5 --streams 16 --steps 6 --warmup 5 --no-e2e --no-cpu-baseline \
   > $OUT/ncu_full_${TAG}c5.log 2>&1; echo "ncu C5 rc=$?"
 for f in C5 C4p C4pf C4mc C5b_g1 C5b_g8; do tail -1 $OUT/bench_${TAG}_$f.json | cut -c1-160; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:dmsgm_prefilter -s 3 -c 1 \
+  -o $OUT/prof_${TAG}pf -f python bench.py --prefilter 5,1.0,1 --steps 4 --warmup 3 --no-e2e --no-cpu-baseline \
+  > $OUT/ncu_full_${TAG}pf.log 2>&1; echo "ncu prefilter rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:dmsgm_warp -s 4 -c 1 \
+  -o $OUT/prof_${TAG}warp -f python bench.py --motion frame --steps 4 --warmup 5 --no-e2e --no-cpu-baseline \
+  > $OUT/ncu_full_${TAG}warp.log 2>&1; echo "ncu warp rc=$?"
