@@ -68,13 +68,20 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_instructions(name):
-    """warp-instructions per launch of a kernel from the committed ncu capture (profiles/), or None."""
+def ncu_instructions(name, pixels=None):
+    """warp-instructions per launch of a kernel from the committed ncu capture (profiles/), or None.
+    Without a capture for this workload, the C4 capture scaled by the pixel count (the
+    filter and warp kernels do the same work per pixel) when `pixels` is given."""
     try:
         with open(os.path.join(ROOT, "profiles", f"ncu_instr_{name}.json")) as f:
             return float(json.load(f)["warp_instructions_per_launch"])
     except Exception:
+        pass
+    kernel = name.split("_")[0]
+    if pixels is None or name == f"{kernel}_C4":
         return None
+    c4 = ncu_instructions(f"{kernel}_C4")
+    return c4 * pixels / (32 * 1920 * 1080) if c4 else None
 
 
 def ncu_traffic(workload):
@@ -385,7 +392,7 @@ def run_dmsgm(args, rank, world, local):
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965
         peak_issue = sms * 4 * mhz * 1e6 / 1e9          # warp-instructions / ns (4 schedulers per SM)
-        instr = ncu_instructions(f"prefilter_{args.config}")
+        instr = ncu_instructions(f"prefilter_{args.config}", pixels=S * W * H)
         pf_roof = {"bound": "alu", "unit": "G warp-inst/s", "peak": peak_issue,
                    "achieved": instr / (pf_ms * 1e-3) / 1e9 if instr else None,
                    "frac": instr / (pf_ms * 1e-3) / 1e9 / peak_issue if instr else None,
@@ -413,7 +420,7 @@ def run_dmsgm(args, rank, world, local):
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965
         peak_issue = sms * 4 * mhz * 1e6 / 1e9          # warp-instructions / ns (4 schedulers per SM)
-        instr = ncu_instructions(f"warp_{args.config}")
+        instr = ncu_instructions(f"warp_{args.config}", pixels=S * W * H)
         warp_roof = {"bound": "alu", "unit": "G warp-inst/s", "peak": peak_issue,
                      "achieved": instr / (w_ms * 1e-3) / 1e9 if instr else None,
                      "frac": instr / (w_ms * 1e-3) / 1e9 / peak_issue if instr else None,
@@ -453,11 +460,11 @@ def run_dmsgm(args, rank, world, local):
             "gpu_launches": info.kernels_per_step * args.steps,
             "clocks": clocks,
         }
-        # with preprocessing and/or frame warping the dominant kernel of the step is the
-        # (ALU-bound) filter or warp kernel: it becomes `roofline`; the HBM figure of the
-        # whole step is kept as roofline_step
+        # with preprocessing and/or frame warping the dominant kernel of the step can be the
+        # (ALU-bound) filter or warp kernel: if one takes half the step or more it becomes
+        # `roofline` and the HBM figure of the whole step is kept as roofline_step
         extra = [r for r in (pf_roof, warp_roof) if r]
-        if extra:
+        if extra and max(r["share_of_step"] for r in extra) >= 0.5:
             line["roofline_step"] = line["roofline"]
             line["roofline"] = max(extra, key=lambda r: r["share_of_step"])
         if pf_roof:

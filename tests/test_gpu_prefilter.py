@@ -14,7 +14,10 @@ COMBOS = [(1, 1.0, 0), (1, 1.0, 1), (3, 1.0, 0), (3, 0.8, 1), (5, 1.0, 0), (5, 1
 
 
 @pytest.mark.parametrize("gs,sigma,mr", COMBOS)
-@pytest.mark.parametrize("W,H,S", [(4, 1, 1), (8, 3, 2), (100, 45, 2), (256, 64, 1), (132, 33, 3)])
+# sizes: single pixel rows, ragged 120-column strips and 40-row bands of the streaming
+# kernel (244 = 2 x 120 + 4, 81 = 2 x 40 + 1), a 1080p-wide frame of 2 rows
+@pytest.mark.parametrize("W,H,S", [(4, 1, 1), (8, 3, 2), (100, 45, 2), (256, 64, 1), (132, 33, 3), (244, 81, 1),
+                                   (1920, 2, 1), (364, 121, 2)])
 def test_filter_bitwise(cuda_lib, oracle_mod, gs, sigma, mr, W, H, S):
     import torch
     rng = np.random.default_rng(W * 1000 + H + gs + mr)
@@ -41,6 +44,9 @@ def test_filter_argument_errors(cuda_lib):
     for bad in [(4, 1.0, 1), (9, 1.0, 0), (5, 0.0, 1), (5, 1.0, 2)]:
         with pytest.raises(cuda_lib.DmsgmError):
             cuda_lib.prefilter(x, x, *bad)
+    y = torch.zeros((1, 8, 18), dtype=torch.uint8, device="cuda")[..., :16]   # row pitch 18: not 4-byte aligned
+    with pytest.raises(cuda_lib.DmsgmError):
+        cuda_lib.prefilter(y, x, 5, 1.0, 1)
 
 
 def _run_step_with_prefilter(dm, frames, Hs, N, params, mode):
