@@ -302,7 +302,7 @@ cudaError_t launch_warp(int W, int H, int count, const uint8_t* in, long long in
     a.in = in; a.in_stride = in_stride; a.in_pitch = (int)in_pitch;
     a.out = out; a.out_stride = out_stride; a.out_pitch = (int)out_pitch;
     a.H = Hs; a.W = W; a.Hh = H; a.count = count;
-    // persistent: up to 4 CTAs per SM (registers and the two 24 KB source-box stages)
+    // persistent: kWarpCtasPerSm CTAs per SM
     // (per device: the dynamic shared-memory opt-in is a per-device function attribute)
     static int sms_of[64] = {0};
     int dev = 0;
@@ -317,7 +317,8 @@ cudaError_t launch_warp(int W, int H, int count, const uint8_t* in, long long in
     }
     const long long tiles = (long long)((W / 4 + kWarpThreadsX - 1) / kWarpThreadsX) *
                             ((H + kWarpTileY - 1) / kWarpTileY) * count;
-    const int grid = (int)(tiles < 4LL * sms ? tiles : 4LL * sms);
+    const long long resident = (long long)kWarpCtasPerSm * sms;   // every CTA resident: contiguous tile ranges
+    const int grid = (int)(tiles < resident ? tiles : resident);
     if (grid == 0) return cudaSuccess;
     dmsgm_warp_kernel<<<grid, kWarpThreads, kWarpDynSmem, stream>>>(a);
     return cudaGetLastError();
