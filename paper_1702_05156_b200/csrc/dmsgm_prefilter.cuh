@@ -101,10 +101,16 @@ constexpr int kPfOutW = 120;      // output columns per warp (lanes 1..30)
 #define DMSGM_PF_BAND 40
 #endif
 constexpr int kPfBand = DMSGM_PF_BAND;   // output rows per warp (A/B at C4: 32/40/48/64 rows -> 117.6/115.1/119.0/121.2 us)
-constexpr int kPfWarps = 8;       // warps per CTA (independent strips)
+#ifndef DMSGM_PF_WARPS
+#define DMSGM_PF_WARPS 8
+#endif
+#ifndef DMSGM_PF_MINB
+#define DMSGM_PF_MINB 1
+#endif
+constexpr int kPfWarps = DMSGM_PF_WARPS;   // warps per CTA (independent strips)
 
 template <int G, int M>
-__global__ void __launch_bounds__(32 * kPfWarps) dmsgm_prefilter_kernel(const PrefilterArgs a) {
+__global__ void __launch_bounds__(32 * kPfWarps, DMSGM_PF_MINB) dmsgm_prefilter_kernel(const PrefilterArgs a) {
     constexpr int NR = 2 * G + 1;                   // column-pass ring (rows in flight)
     const int lane = threadIdx.x & 31;
     const int strip = blockIdx.x * kPfWarps + (threadIdx.x >> 5);
