@@ -113,3 +113,77 @@ def test_extreme_sizes(cuda_lib, oracle_mod, W, H, N, S, T, monkeypatch):
     compare_state(gst, os_[T - 1], where=f"{W}x{H} N={N} S={S}")
     compare_masks(gm[T - 1], om[T - 1], frames[T - 1], (os_[T - 1][:, 0], os_[T - 1][:, 1]), N, where="last frame")
     assert np.mean(gm == om) > 0.9999                      # earlier frames (states not snapshotted)
+
+
+@pytest.mark.parametrize("prefilter,frame_warp", [((5, 1.0, 1), False), (None, True), ((5, 1.0, 1), True)])
+def test_fullsize_paper_modes(cuda_lib, oracle_mod, prefilter, frame_warp, monkeypatch):
+    """The bench's C4 launch configuration (32 x 1080p, N=4) with the paper's own
+    preprocessing (NEXT-2) and/or frame-warp motion compensation (NEXT-3): every CTA of
+    the persistent warp kernel walks ~20 tiles (plan-ring wrap, stream changes inside a
+    CTA's range) and the streaming filter covers the whole batch.  Sampled streams against
+    the oracle run as filter -> warp -> step with H = I (R34, R35)."""
+    monkeypatch.delenv("DMSGM_KERNEL", raising=False)
+    import torch
+    dm = cuda_lib
+    sample = [0, 13, 31]
+    T = 3
+    cfg = synth.config("C4", T=T)
+    seq = synth.generate(cfg, streams=sample)
+    S, H, W, N = cfg.S, cfg.H, cfg.W, cfg.N
+    src = [sample.index(s) if s in sample else s % len(sample) for s in range(S)]
+    pg, _ = params_pair(dm, oracle_mod, S)
+    ctx = dm.Dmsgm(W, H, N, pg)
+    if prefilter:
+        ctx.set_prefilter(*prefilter)
+    if frame_warp:
+        ctx.set_motion(dm.DMSGM_MC_FRAME)
+    frames = seq.frames if not prefilter else oracle_mod.prefilter_frames(seq.frames, *prefilter)
+    if frame_warp:
+        frames = oracle_mod.warp_frames(frames, seq.homographies)
+        homs = np.broadcast_to(np.eye(3).reshape(9), seq.homographies.shape).copy()
+    else:
+        homs = seq.homographies
+    o = oracle_mod.Oracle(W, H, N, params_pair(dm, oracle_mod, len(sample))[1])
+    f = torch.empty((S, H, W), dtype=torch.uint8, device="cuda")
+    m = torch.empty_like(f)
+    for t in range(T):
+        f.copy_(torch.from_numpy(seq.frames[t][src]))
+        h = torch.from_numpy(np.ascontiguousarray(seq.homographies[t][src])).cuda()
+        ctx.step(f, h, m)
+        om = o.step(frames[t], homs[t])
+        torch.cuda.synchronize()
+        gm = m.cpu().numpy()
+        ost = np.stack([o.get_state(j) for j in range(len(sample))])
+        gst = np.stack([ctx.get_state(s) for s in sample])
+        where = f"C4 prefilter={prefilter} frame_warp={frame_warp} t={t}"
+        compare_state(gst, ost, where=where)
+        compare_masks(gm[sample], om, frames[t], (ost[:, 0], ost[:, 1]), N, where=where)
+    ctx.close()
+    o.close()
+
+
+def test_fullsize_warp_and_filter_kernels(cuda_lib, oracle_mod):
+    """The stand-alone warp and filter kernels over the whole C4 batch (32 x 1080p, the
+    bench's grid), every stream bitwise against the oracle."""
+    import torch
+    cfg = synth.config("C4", T=1)
+    sample = [0, 9, 22]
+    seq = synth.generate(cfg, streams=sample)
+    S = cfg.S
+    src = [sample.index(s) if s in sample else s % len(sample) for s in range(S)]
+    fr = seq.frames[0][src]
+    hs = np.ascontiguousarray(seq.homographies[0][src])
+    f = torch.from_numpy(fr).cuda()
+    out = torch.empty_like(f)
+    cuda_lib.warp_frames(f, torch.from_numpy(hs).cuda(), out)
+    torch.cuda.synchronize()
+    want = oracle_mod.warp_frames(seq.frames[0], seq.homographies[0])
+    got = out.cpu().numpy()
+    for s in range(S):
+        assert np.array_equal(got[s], want[src[s]]), f"warp stream {s}: {(got[s] != want[src[s]]).sum()} px differ"
+    cuda_lib.prefilter(f, out, 5, 1.0, 1)
+    torch.cuda.synchronize()
+    want = oracle_mod.prefilter_frames(seq.frames[0], 5, 1.0, 1)
+    got = out.cpu().numpy()
+    for s in range(S):
+        assert np.array_equal(got[s], want[src[s]]), f"filter stream {s}: {(got[s] != want[src[s]]).sum()} px differ"
