@@ -260,10 +260,16 @@ def run_dmsgm(args, rank, world, local):
     import synth
     from paper_1702_05156_b200.shard import max_over_ranks, strong_shard, weak_shard
 
+    if args.same_device:          # functional check of the torchrun path on a 1-GPU box
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
+    red_dev = dev if args.dist_backend == "nccl" else None
     wl = WORKLOADS[args.config]
     base = synth.config(wl["ring"])
     if args.streams:
@@ -318,7 +324,7 @@ def run_dmsgm(args, rank, world, local):
     if world > 1:
         dist.barrier()
     ms_local = ev0.elapsed_time(ev1)
-    ms = max_over_ranks(ms_local, dev)                     # the slowest rank sets the job time
+    ms = max_over_ranks(ms_local, red_dev)                     # the slowest rank sets the job time
     ms_per_step = ms / args.steps
     total_streams = world * base.S if args.scaling == "weak" else base.S
     frames_total = total_streams * args.steps
@@ -350,7 +356,7 @@ def run_dmsgm(args, rank, world, local):
             # uploads overlap step i's downloads; one sync ends the timed region.
             ctx.step_host_async(ring_host[i % len(ring_host)], hH[i % RING], hm2[i % 2], stream)
         torch.cuda.synchronize(dev)
-        e2e_s = max_over_ranks(time.perf_counter() - t0, dev)
+        e2e_s = max_over_ranks(time.perf_counter() - t0, red_dev)
         e2e = {"value": total_streams * e2e_steps / e2e_s, "unit": "frames/s",
                "h2d_bytes_per_step": S * H * W + S * 9 * 8, "d2h_bytes_per_step": S * H * W,
                "steps": e2e_steps,
@@ -698,8 +704,8 @@ def main():
     ap.add_argument("--motion", default="models", choices=["models", "frame"],
                     help="motion compensation: warp the models (default, north_star) or the frame (App. F, NEXT-3)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
-                    help="C5b: process-group backend (gloo + --same-device: functional test on one GPU)")
-    ap.add_argument("--same-device", action="store_true", help="C5b: every rank on cuda:0 (testing only)")
+                    help="process-group backend (gloo + --same-device: functional test of the torchrun path on one GPU)")
+    ap.add_argument("--same-device", action="store_true", help="every rank on cuda:0 (testing only)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
