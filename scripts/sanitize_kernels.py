@@ -1,0 +1,36 @@
+"""Small invocations of the frame-warp, prefilter and step kernels for compute-sanitizer
+(memcheck / racecheck / synccheck): python scripts/sanitize_kernels.py"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import synth                                        # noqa: E402
+from paper_1702_05156_b200 import dmsgm as dm       # noqa: E402
+
+rng = np.random.default_rng(3)
+S, H, W = 3, 100, 700                               # ragged tiles, several tiles per CTA
+fr = torch.from_numpy(rng.integers(0, 256, (S, H, W), dtype=np.uint8)).cuda()
+hs = np.stack([synth.random_homography(rng, W, H, shift=5, rot_deg=2, zoom=0.02, persp=1e-5) for _ in range(S)])
+hs[1] = [1, 0, -40.5, 0, 1, 7.25, 0, 0, 1]          # border tiles far outside the frame
+out = torch.empty_like(fr)
+dm.warp_frames(fr, torch.from_numpy(hs).cuda(), out)
+dm.prefilter(fr, out, 5, 1.0, 1)
+cfg = synth.config("C2", T=3, S=2)
+seq = synth.generate(cfg)
+p = dict(theta_s=4.0, theta_d=4.0, var_init=255.0, age_cap=30.0, var_floor_match=0.1, var_floor_classify=0.25,
+         decay_lambda=0.001, decay_var_thresh=2500.0, num_streams=cfg.S)
+for mode in (dm.DMSGM_MC_MODELS, dm.DMSGM_MC_FRAME):
+    ctx = dm.Dmsgm(cfg.W, cfg.H, cfg.N, dm.Params(**p))
+    ctx.set_motion(mode)
+    if mode == dm.DMSGM_MC_FRAME:
+        ctx.set_prefilter(5, 1.0, 1)
+    f = torch.from_numpy(seq.frames).cuda()
+    h = torch.from_numpy(seq.homographies).cuda()
+    m = torch.zeros_like(f)
+    for t in range(cfg.T):
+        ctx.step(f[t], h[t], m[t])
+    ctx.close()
+torch.cuda.synchronize()
+print("sanitize run ok")
