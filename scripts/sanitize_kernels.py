@@ -1,5 +1,6 @@
-"""Small invocations of the frame-warp, prefilter and step kernels for compute-sanitizer
-(memcheck / racecheck / synccheck): python scripts/sanitize_kernels.py"""
+"""Small invocations of the frame-warp, prefilter and step kernels (every block size, both
+step kernels) for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
+python scripts/sanitize_kernels.py"""
 import sys
 
 import numpy as np
@@ -32,5 +33,22 @@ for mode in (dm.DMSGM_MC_MODELS, dm.DMSGM_MC_FRAME):
     for t in range(cfg.T):
         ctx.step(f[t], h[t], m[t])
     ctx.close()
+# every block size (staged kernels for N = 1, 2, 4, 8; the register-path kernel for N = 16
+# and, forced, for N = 4) on random near-identity motion
+import os                                            # noqa: E402
+for N, generic in [(1, False), (2, False), (8, False), (16, False), (4, True)]:
+    if generic:
+        os.environ["DMSGM_KERNEL"] = "generic"
+    Wn, Hn, Sn = 16 * 17, 16 * 5, 2
+    pn = dict(p, num_streams=Sn)
+    ctx = dm.Dmsgm(Wn, Hn, N, dm.Params(**pn))
+    f = torch.from_numpy(rng.integers(0, 256, (3, Sn, Hn, Wn), dtype=np.uint8)).cuda()
+    h = torch.from_numpy(np.stack([[synth.random_homography(rng, Wn, Hn, shift=3, rot_deg=1, zoom=0.01, persp=1e-5)
+                                    for _ in range(Sn)] for _ in range(3)])).cuda()
+    m = torch.zeros_like(f)
+    for t in range(3):
+        ctx.step(f[t], h[t], m[t])
+    ctx.close()
+    os.environ.pop("DMSGM_KERNEL", None)
 torch.cuda.synchronize()
 print("sanitize run ok")
