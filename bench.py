@@ -36,6 +36,7 @@ if ROOT not in sys.path:
 L2_BYTES = 126 * 1024 * 1024
 RING = 8
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
+SPEC_HBM_GBS = 8000.0       # B200 datasheet HBM3e bandwidth: BASELINE.md §3's denominator, reported beside
 
 WORKLOADS = {
     "C4": dict(ring="C4ring", desc="1920x1080 u8, 4x4 blocks, 32 streams/GPU"),
@@ -456,6 +457,7 @@ def run_dmsgm(args, rank, world, local):
                        "parallelism": f"stream-sharded x{world}, no data-path collective"},
             "mpixel_per_s": fps * W * H / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "spec_peak": SPEC_HBM_GBS, "frac_of_spec": achieved / SPEC_HBM_GBS,
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_step,
                          "peak_source": peak_src,
@@ -664,6 +666,7 @@ def run_band(args, rank, world, local):
                        "parallelism": f"row bands x{G} of one stream"},
             "mpixel_per_s": fps * W * H / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "spec_peak": SPEC_HBM_GBS, "frac_of_spec": achieved / SPEC_HBM_GBS,
                          "frac": achieved / peak, "traffic": None,
                          "algorithmic_bytes_per_launch": bytes_per_step, "peak_source": peak_src,
                          "kernel": f"{kernel_name} x{len(ctxs)} + band sync",
