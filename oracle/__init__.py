@@ -22,7 +22,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dmsgm_oracle.c")
 _SRC2 = os.path.join(_HERE, "prefilter_oracle.c")
 _SRC3 = os.path.join(_HERE, "warp_oracle.c")
+_SRC4 = os.path.join(_HERE, "dmsgm_plain.c")
 _HDR = os.path.join(_HERE, "dmsgm_oracle.h")
+_HDR2 = os.path.join(_HERE, "oracle_ctx.h")
 LIB_PATH = os.path.join(_HERE, "libdmsgm_oracle.so")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
           "-Wall", "-Wextra"]
@@ -33,10 +35,10 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile the oracle into oracle/libdmsgm_oracle.so (gcc, no FMA contraction)."""
-    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC2), os.path.getmtime(_SRC3), os.path.getmtime(_HDR))
+    newest = max(os.path.getmtime(f) for f in (_SRC, _SRC2, _SRC3, _SRC4, _HDR, _HDR2))
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
         tmp = LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC2, _SRC3, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC4, _SRC2, _SRC3, "-lm"])
         os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
@@ -47,7 +49,10 @@ class _Params(ctypes.Structure):
                 ("var_floor_match", ctypes.c_float), ("var_floor_classify", ctypes.c_float),
                 ("decay_lambda", ctypes.c_float), ("decay_var_thresh", ctypes.c_float),
                 ("num_streams", ctypes.c_int), ("update_rule", ctypes.c_int),
-                ("classify_rule", ctypes.c_int)]
+                ("classify_rule", ctypes.c_int), ("form", ctypes.c_int)]
+
+FORM_KERNEL_ORDER = 0   # dmsgm_oracle.c: the canonical fp32 order the CUDA path reproduces bitwise
+FORM_PLAIN = 1          # dmsgm_plain.c: SURVEY §8(c)'s literal definition (fp64 projection, / sum W, libm exp)
 
 
 def _load():
@@ -69,8 +74,9 @@ def _load():
             lib.dmsgm_oracle_set_state.argtypes = [P, i32, P]
             lib.dmsgm_oracle_is_initialised.argtypes = [P, i32]
             lib.dmsgm_oracle_mix_weights.argtypes = [i32, i32, i32, P, i32, i32, P, P, P, P]
-            lib.dmsgm_oracle_decay_exp.argtypes = [ctypes.c_float]
-            lib.dmsgm_oracle_decay_exp.restype = ctypes.c_float
+            lib.dmsgm_oracle_decay_factor.argtypes = [ctypes.c_float, ctypes.c_float]
+            lib.dmsgm_oracle_decay_factor.restype = ctypes.c_float
+            lib.dmsgm_oracle_set_tilde_probe.argtypes = [P, P]
             lib.dmsgm_oracle_gauss_taps.argtypes = [i32, ctypes.c_float, P]
             lib.dmsgm_oracle_prefilter.argtypes = [i32, i32, P, sz, P, sz, i32, ctypes.c_float, i32]
             lib.dmsgm_oracle_warp_frame.argtypes = [i32, i32, P, sz, P, P, sz]
@@ -91,12 +97,13 @@ class OracleParams:
     num_streams: int = 1
     update_rule: int = 0
     classify_rule: int = 0
+    form: int = FORM_KERNEL_ORDER
 
     def _c(self) -> _Params:
         return _Params(self.theta_s, self.theta_d, self.var_init, self.age_cap,
                        self.var_floor_match, self.var_floor_classify, self.decay_lambda,
                        self.decay_var_thresh, self.num_streams, self.update_rule,
-                       self.classify_rule)
+                       self.classify_rule, self.form)
 
 
 def _ptr(a: np.ndarray):
@@ -165,13 +172,22 @@ class Oracle:
         if self.lib.dmsgm_oracle_set_state(self._h, stream, _ptr(st)) != 0:
             raise ValueError("bad stream")
 
+    def set_tilde_probe(self, on: bool = True):
+        """While on, every step records per block the tilde models after S1-S3, M and a
+        live flag into self.tilde [S][8][Hb][Wb] (test probe)."""
+        if on:
+            self.tilde = np.zeros((self.S, 8, self.Hb, self.Wb), np.float32)
+            self.lib.dmsgm_oracle_set_tilde_probe(self._h, _ptr(self.tilde))
+        else:
+            self.lib.dmsgm_oracle_set_tilde_probe(self._h, None)
+
     def is_initialised(self, stream: int) -> bool:
         return bool(self.lib.dmsgm_oracle_is_initialised(self._h, stream))
 
 
-def decay_exp(x: float) -> float:
-    """exp(-x) as the oracle evaluates it (reading R18)."""
-    return float(_load().dmsgm_oracle_decay_exp(x))
+def decay_factor(lam: float, d: float) -> float:
+    """exp(-lam * d) as the kernel-order form evaluates it (reading R18), lam and d fp32."""
+    return float(_load().dmsgm_oracle_decay_factor(lam, d))
 
 
 def gauss_taps(size: int, sigma: float) -> np.ndarray:

@@ -26,33 +26,15 @@
  * Layout: state [S][6][Hb][Wb] fp32, planes mu_A var_A age_A mu_C var_C age_C.
  */
 #include "dmsgm_oracle.h"
+#include "oracle_ctx.h"
 
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
-struct dmsgm_oracle_ctx {
-    int W, H, N, Wb, Hb, S;
-    dmsgm_oracle_params p;
-    float* state[2];            /* [S][6][Hb][Wb] */
-    int cur;                    /* state[cur] holds the models after frame t-1 */
-    unsigned char* initialised; /* [S] */
-};
+static size_t plane_elems(const dmsgm_oracle_ctx* c) { return oracle_plane_elems(c); }
 
-/* One single Gaussian model: mean mu, variance sigma, age alpha (§2.2). */
-typedef struct {
-    float mu;
-    float var;
-    float age;
-} sgm;
-
-enum { P_MU_A = 0, P_VAR_A, P_AGE_A, P_MU_C, P_VAR_C, P_AGE_C, P_NUM };
-
-static size_t plane_elems(const dmsgm_oracle_ctx* c) { return (size_t)c->Wb * (size_t)c->Hb; }
-
-static float* stream_state(const dmsgm_oracle_ctx* c, int buf, int s) {
-    return c->state[buf] + (size_t)s * P_NUM * plane_elems(c);
-}
+static float* stream_state(const dmsgm_oracle_ctx* c, int buf, int s) { return oracle_stream_state(c, buf, s); }
 
 /* ------------------------------------------------------------------------
  * S1: project the block centre through H and find the up-to-4 source blocks
@@ -118,17 +100,21 @@ static int project_block(int Wb, int Hb, int N, const double* h, int bi, int bj,
 }
 
 /* ------------------------------------------------------------------------
- * R18: exp(-x) for x >= 0 in fp32 by one fixed sequence of IEEE operations
- * (so that any two IEEE machines agree bitwise):
- *   n = rint(x * log2 e);  r = fma(-n, L1, x); r = fma(-n, L2, r)   (L1 + L2 = ln 2;
- *   L1 has 16 significant bits, so n*L1 is exact for n < 128);
+ * R18: the decay factor exp(-lambda * d), d = var~ - theta_v >= 0, in fp32 by one fixed
+ * sequence of IEEE operations (so that any two IEEE machines agree bitwise), accurate
+ * to about one fp32 ulp of the plain form's (float) exp(-(double) lambda * (double) d):
+ *   x = lambda * d exactly as xh + xl (xh = fl(lambda d), xl = fma(lambda, d, -xh));
+ *   n = rint(xh * log2 e);  r = fma(-n, L1, xh) + xl;  r = fma(-n, L2, r)
+ *     (L1 + L2 = ln 2; L1 has 16 significant bits, so n*L1 is exact for n < 128);
  *   p = sum_{k=0..7} (-r)^k / k!  by Horner with fma from k = 7 down;  exp(-x) = p * 2^-n.
- * x >= 86 returns 0 (exp(-86) is within 3 binades of FLT_MIN).
+ * xh >= 86 returns 0 (exp(-86) is within 3 binades of FLT_MIN).
  * ---------------------------------------------------------------------- */
-static float decay_exp(float x) {
-    if (!(x < 86.0f)) return 0.0f;
-    const float n = rintf(x * 1.44269502f);
-    float r = fmaf(-n, 0.693145751953125f, x);
+static float decay_factor(float lambda, float d) {
+    const float xh = lambda * d;
+    const float xl = fmaf(lambda, d, -xh);
+    if (!(xh < 86.0f)) return 0.0f;
+    const float n = rintf(xh * 1.44269502f);
+    float r = fmaf(-n, 0.693145751953125f, xh) + xl;
     r = fmaf(-n, 1.42860677e-06f, r);
     float p = -1.98412701e-04f;            /* -1/7! */
     p = fmaf(p, r, 1.38888892e-03f);       /*  1/6! */
@@ -151,7 +137,7 @@ static float decay_exp(float x) {
  * Sums run over in-range sources in the order self, H, V, HV, accumulated with
  * fused multiply-adds acc = fma(w_k, x_k, acc) from acc = 0 (R17).
  * S3: age decay (R7): if lambda > 0 and var~ > theta_v,
- *   age~ <- age~ * exp(-lambda (var~ - theta_v))   with exp as in decay_exp (R18).
+ *   age~ <- age~ * exp(-lambda (var~ - theta_v))   with exp as in decay_factor (R18).
  * ---------------------------------------------------------------------- */
 static sgm mix_model(const dmsgm_oracle_ctx* c, const float* prev, int pm, const int kx[4],
                      const int ky[4], const float wn[4], const int valid[4]) {
@@ -187,8 +173,7 @@ static sgm mix_model(const dmsgm_oracle_ctx* c, const float* prev, int pm, const
     /* S3 */
     if (c->p.decay_lambda > 0.0f && m.var > c->p.decay_var_thresh) {
         float excess = m.var - c->p.decay_var_thresh;
-        float x = c->p.decay_lambda * excess;
-        m.age = m.age * decay_exp(x);
+        m.age = m.age * decay_factor(c->p.decay_lambda, excess);
     }
     return m;
 }
@@ -228,13 +213,15 @@ static sgm update_model(const dmsgm_oracle_ctx* c, sgm t, float M, const uint8_t
         r.mu = keep * t.mu + alpha * M;                                  /* P:608 */
         float V = block_V(r.mu, frame, pitch, x0, y0, c->N);             /* P:609 */
         r.var = keep * t.var + alpha * V;                                /* P:610 */
-        r.age = t.age < c->p.age_cap ? t.age + 1.0f : t.age;             /* P:616-618 */
+        float den = t.age + 1.0f;                                        /* P:616-618 with R22: */
+        r.age = den < c->p.age_cap ? den : c->p.age_cap;                 /* min(age~+1, cap) */
     }
     return r;
 }
 
 static int step_stream(dmsgm_oracle_ctx* c, int s, const uint8_t* frame, size_t fpitch,
                        const double* h, uint8_t* mask, size_t mpitch) {
+    if (c->p.form == DMSGM_ORACLE_FORM_PLAIN) return dmsgm_plain_step_stream(c, s, frame, fpitch, h, mask, mpitch);
     const int N = c->N, Wb = c->Wb, Hb = c->Hb;
     const size_t pe = plane_elems(c);
     const float* prev = stream_state(c, c->cur, s);
@@ -268,6 +255,7 @@ static int step_stream(dmsgm_oracle_ctx* c, int s, const uint8_t* frame, size_t 
                     Ct = mix_model(c, prev, P_MU_C, kx, ky, wn, valid);
                 }
             }
+            if (c->dump) oracle_dump_tilde(c, s, bj, bi, At, Ct, M, !exposed);   /* test probe only */
             if (exposed) {
                 /* S0 / R8: A = C = (M, var_init, 1); no update this frame */
                 A.mu = M; A.var = c->p.var_init; A.age = 1.0f;
@@ -335,6 +323,7 @@ static int params_ok(const dmsgm_oracle_params* p) {
     if (!(p->decay_lambda >= 0.0f) || !(p->decay_var_thresh >= 0.0f)) return 0;
     if (p->num_streams < 1) return 0;
     if (p->update_rule < 0 || p->update_rule > 1 || p->classify_rule < 0 || p->classify_rule > 1) return 0;
+    if (p->form != DMSGM_ORACLE_FORM_KERNEL_ORDER && p->form != DMSGM_ORACLE_FORM_PLAIN) return 0;
     return 1;
 }
 
@@ -433,4 +422,10 @@ int dmsgm_oracle_mix_weights(int width, int height, int block, const double* h, 
     return r ? 1 : (clipped ? 2 : 0);
 }
 
-float dmsgm_oracle_decay_exp(float x) { return decay_exp(x); }
+int dmsgm_oracle_set_tilde_probe(dmsgm_oracle_ctx* c, float* buf) {
+    if (!c) return -1;
+    c->dump = buf;
+    return 0;
+}
+
+float dmsgm_oracle_decay_factor(float lambda, float d) { return decay_factor(lambda, d); }

@@ -34,7 +34,13 @@ typedef struct {
     int   num_streams;        /* S                                                     */
     int   update_rule;        /* 0 = Eqs. 3/5/7 (R10); 1 = App. E code rule (R27)      */
     int   classify_rule;      /* 0 = theta_d*max(var_A,f_c) (R14); 1 = App. E theta_d*max(f_c,I) (R28) */
+    int   form;               /* arithmetic form: DMSGM_ORACLE_FORM_KERNEL_ORDER (dmsgm_oracle.c, the
+                                 canonical fp32 order the CUDA path reproduces bitwise) or
+                                 DMSGM_ORACLE_FORM_PLAIN (dmsgm_plain.c, SURVEY §8(c) literally) */
 } dmsgm_oracle_params;
+
+#define DMSGM_ORACLE_FORM_KERNEL_ORDER 0
+#define DMSGM_ORACLE_FORM_PLAIN 1
 
 typedef struct dmsgm_oracle_ctx dmsgm_oracle_ctx;
 
@@ -70,8 +76,13 @@ int dmsgm_oracle_is_initialised(const dmsgm_oracle_ctx* ctx, int stream);
 int dmsgm_oracle_mix_weights(int width, int height, int block, const double* h, int bi, int bj,
                              int* src_x, int* src_y, float* weight, float* sum_w);
 
-/* The decay factor exp(-x) of reading R18 (exposed for its pin). */
-float dmsgm_oracle_decay_exp(float x);
+/* Test probe: while buf is set, every step also writes, per stream and block, the tilde
+ * models after S1-S3 (mu~_A var~_A age~_A mu~_C var~_C age~_C), the block mean M and
+ * 1/0 for live/exposed into buf [S][8][Hb][Wb] (host memory owned by the caller). */
+int dmsgm_oracle_set_tilde_probe(dmsgm_oracle_ctx* ctx, float* buf);
+
+/* The decay factor exp(-lambda * d) of reading R18 (form 0; exposed for its pin). */
+float dmsgm_oracle_decay_factor(float lambda, float d);
 
 /* Frame preprocessing of §2.1 / §3.3.1 / App. A-B (prefilter_oracle.c, readings R30-R34):
  * the normalised Gaussian taps (size odd <= 15, sigma > 0), and the separable Gaussian

@@ -21,6 +21,7 @@ the DMSGM method.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field, replace
 from typing import Optional
 
@@ -415,12 +416,22 @@ def generate(cfg, T: Optional[int] = None, streams=None, with_gt: bool = False) 
     frames = np.empty((T, len(streams), cfg.H, cfg.W), np.uint8)
     Hs = np.empty((T, len(streams), 9))
     gts = np.empty((T, len(streams), cfg.H, cfg.W), np.uint8) if with_gt else None
+    jobs = []
     for j, s in enumerate(streams):
         sp = _stream_params(cfg, s)
         Hs[:, j] = homographies_for_stream(cfg, s, T, sp)
-        for t in range(T):
-            f, g = render_frame(cfg, sp, t, s, with_gt)
-            frames[t, j] = f
-            if with_gt:
-                gts[t, j] = g
+        jobs += [(j, s, sp, t) for t in range(T)]
+
+    def render(job):
+        j, s, sp, t = job
+        f, g = render_frame(cfg, sp, t, s, with_gt)
+        frames[t, j] = f
+        if with_gt:
+            gts[t, j] = g
+
+    # frames are independent (per-frame noise seeds), so they render in parallel threads
+    # (numpy releases the GIL); the bytes do not depend on the thread count
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1))) as ex:
+        list(ex.map(render, jobs))
     return Sequence(cfg, frames, Hs, gts)
