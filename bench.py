@@ -34,7 +34,8 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 L2_BYTES = 126 * 1024 * 1024
-RING = 8
+RING = 8          # distinct synthetic frames per stream (periodic camera motion, no seam)
+GRAPH_T = 40      # steps per CUDA-graph replay (dmsgm_step_n) in the timed region
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 SPEC_HBM_GBS = 8000.0       # B200 datasheet HBM3e bandwidth: BASELINE.md §3's denominator, reported beside
 
@@ -107,6 +108,7 @@ class ClockSampler:
 
     def __init__(self, device_index):
         self.samples, self.reasons = [], set()
+        self.mem, self.power, self.temp = [], [], []
         self.max_mhz = None
         self._stop = threading.Event()
         self._h = None
@@ -125,6 +127,9 @@ class ClockSampler:
         nv = self.nv
         try:
             self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self.mem.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_MEM))
+            self.power.append(nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0)
+            self.temp.append(nv.nvmlDeviceGetTemperature(self._h, nv.NVML_TEMPERATURE_GPU))
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
             for bit, name in self.REASONS.items():
                 if r & bit and name != "gpu_idle":
@@ -150,8 +155,13 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                     "samples": 0}
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.mem:
+            out.update(mem_mhz_min=min(self.mem), mem_mhz_max=max(self.mem),
+                       power_w_median=float(statistics.median(self.power)), power_w_max=max(self.power),
+                       gpu_temp_c_max=max(self.temp), sm_mhz_min=min(self.samples))
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -188,6 +198,19 @@ def oracle_throughput(cfg, frames_host, Hs, n_streams, n_frames, threads, prefil
     wall = time.perf_counter() - t0
     o.close()
     return n_streams * n_frames / wall, min(threads, n_streams), wall
+
+
+def cpu_model():
+    """The host CPU model (lscpu's "Model name", from /proc/cpuinfo)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cores_available():
@@ -244,6 +267,7 @@ def run_reference(args, rank, world):
                    "streams_per_step": ns},
         "mpixel_per_s": fps * cfg.W * cfg.H / 1e6,
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": min(cores, ns), "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"{ns} streams x 1 frame per step, {args.steps} timed steps, plain C oracle "
                                    f"(-O2, single-threaded per stream, one thread per stream)"},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -282,8 +306,12 @@ def run_dmsgm(args, rank, world, local):
     S = shard.num_streams
     cfg = synth.config(wl["ring"], S=S, seed=base.seed + shard.first_stream)
     W, H, N = cfg.W, cfg.H, cfg.N
-    frames, Hs = synth.generate_device(cfg, T=RING, device=f"cuda:{local}")    # [R][S][H][W] on device
-    Hs_dev = torch.from_numpy(np.ascontiguousarray(Hs)).to(dev)
+    ring, Hs = synth.generate_device(cfg, T=RING, device=f"cuda:{local}")      # [R][S][H][W] on device
+    # the timed steps run as CUDA-graph replays of dmsgm_step_n over GRAPH_T consecutive
+    # frame slots: the ring repeated GRAPH_T / RING times (distinct buffers, > L2)
+    frames = ring.repeat(GRAPH_T // RING, 1, 1, 1)
+    del ring
+    Hs_dev = torch.from_numpy(np.ascontiguousarray(np.tile(Hs, (GRAPH_T // RING, 1, 1)))).to(dev)
     masks = torch.empty_like(frames)
     params = method_params(dm, S)
     ctx = dm.Dmsgm(W, H, N, params, device=local)
@@ -299,32 +327,46 @@ def run_dmsgm(args, rank, world, local):
     bytes_per_step = S * info.algorithmic_bytes_per_frame
 
     def step(i):
-        r = i % RING
+        r = i % GRAPH_T
         ctx.step(frames[r], Hs_dev[r], masks[r], stream)
 
-    # warm-up (first step initialises every stream)
+    # K steps = full replays of the GRAPH_T-step graph + one shorter graph for K % GRAPH_T
+    chunks = [GRAPH_T] * (args.steps // GRAPH_T) + ([args.steps % GRAPH_T] if args.steps % GRAPH_T else [])
+
+    def replay(T):
+        if args.launch == "graph":
+            ctx.step_n(T, frames[:T], Hs_dev[:T], masks[:T], stream)
+        else:                                   # A/B: T single dmsgm_step launches
+            for i in range(T):
+                ctx.step(frames[i], Hs_dev[i], masks[i], stream)
+
+    # warm-up: W single steps (the first initialises every stream), then capture (and run)
+    # the graphs the timed region replays -- untimed
     for i in range(args.warmup):
         step(i)
+    for T in sorted(set(chunks)):
+        replay(T)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(chunks) + 1)]
     sampler = ClockSampler(local)
     with sampler:
         torch.cuda.nvtx.range_push("timed")
-        ev0.record(stream)
-        for i in range(args.steps):
-            step(args.warmup + i)
-        ev1.record(stream)
+        evs[0].record(stream)
+        for k, T in enumerate(chunks):
+            replay(T)
+            evs[k + 1].record(stream)
         torch.cuda.nvtx.range_pop()
         sampler.sample_once()
-        ev1.synchronize()
+        evs[-1].synchronize()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    ms_local = ev0.elapsed_time(ev1)
+    ms_local = evs[0].elapsed_time(evs[-1])
+    rep_ms = [evs[k].elapsed_time(evs[k + 1]) / T for k, T in enumerate(chunks) if T == GRAPH_T]
+    median_ms_per_step = statistics.median(rep_ms) if rep_ms else ms_local / args.steps
     ms = max_over_ranks(ms_local, red_dev)                     # the slowest rank sets the job time
     ms_per_step = ms / args.steps
     total_streams = world * base.S if args.scaling == "weak" else base.S
@@ -376,9 +418,15 @@ def run_dmsgm(args, rank, world, local):
         nf = max(2, int(target_s / per_frame / ns * min(cores, ns)))
         cfps, used, wall = oracle_throughput(cfg, fh, Hs[:2, :ns], ns, nf, cores, prefilter=pf,
                                              frame_warp=args.motion == "frame")
-        cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle",
+        # SURVEY §8(d) oracle timing (i): ONE core, the single-threaded oracle on one stream
+        nf1 = max(2, int(args.cpu_seconds / 3.0 / per_frame))
+        c1fps, _, wall1 = oracle_throughput(cfg, fh[:, :1], Hs[:2, :1], 1, nf1, 1, prefilter=pf,
+                                            frame_warp=args.motion == "frame")
+        cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"{ns} streams x {nf} frames of {wl['desc'].split(',')[0]} (N={N}), "
-                         f"{wall:.1f} s wall, one single-threaded oracle step per stream per thread"}
+                         f"{wall:.1f} s wall, one single-threaded oracle step per stream per thread",
+               "one_core": {"value": c1fps, "unit": "frames/s", "cores": 1,
+                            "sample": f"1 stream x {nf1} frames, {wall1:.1f} s wall, single-threaded oracle"}}
 
     clocks = sampler.summary()
     # NEXT-2 preprocessing: its kernel dominates the step and is ALU-bound -- time it
@@ -444,6 +492,13 @@ def run_dmsgm(args, rank, world, local):
         line = {
             "metric": "frames/s", "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "median_ms_per_step": median_ms_per_step,
+            "replay_ms_per_step": [round(x, 5) for x in rep_ms],
+            "timing": f"{len(chunks)} " + ("CUDA-graph replays of dmsgm_step_n" if args.launch == "graph" else
+                                           "groups of single dmsgm_step launches") + f" ({GRAPH_T} steps each"
+                      f"{'' if args.steps % GRAPH_T == 0 else ', the last ' + str(args.steps % GRAPH_T)}) "
+                      f"between CUDA events on the launching stream; value from the whole K-step region, "
+                      f"median_ms_per_step = median over the {len(rep_ms)} full replays",
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth/ ring recipe, generated on device)",
             "config": {"workload": args.config + ("+prefilter" if pf else "") + ("+framewarp" if args.motion == "frame"
@@ -452,8 +507,9 @@ def run_dmsgm(args, rank, world, local):
                        "N": N, "prefilter": {"gauss_size": pf[0], "gauss_sigma": pf[1], "median_radius": pf[2]}
                        if pf else None,
                        "streams_per_gpu": S, "total_streams": total_streams, "ring_frames": RING,
-                       "l2": f"inputs larger than L2: {bytes_per_step / 1e6:.1f} MB algorithmic traffic per step "
-                             f"(ring of {RING} distinct frames/masks per stream, {2 * RING * S * W * H / 1e9:.2f} GB)",
+                       "l2": f"inputs larger than L2: {bytes_per_step / 1e6:.1f} MB algorithmic traffic per step; "
+                             f"{GRAPH_T} frame + mask slots per stream ({RING} distinct frames repeated), "
+                             f"{2 * GRAPH_T * S * W * H / 1e9:.2f} GB",
                        "parallelism": f"stream-sharded x{world}, no data-path collective"},
             "mpixel_per_s": fps * W * H / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -638,7 +694,7 @@ def run_band(args, rank, world, local):
         per_frame = 0.021 * (W * H) / (1920 * 1080) * (0.4 + 9.6 / N ** 2)   # oracle s/frame (per-block work ~ 1/N^2)
         nf = max(2, int(args.cpu_seconds / per_frame))
         cfps, used, wall = oracle_throughput(cfg, seq.frames, seq.homographies, 1, nf, 1)
-        cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle",
+        cpu = {"value": cfps, "unit": "frames/s", "cores": used, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"1 stream x {nf} frames of 3840x2160 (N={N}), whole frame, {wall:.1f} s wall, "
                          f"single-threaded oracle"}
     clocks = sampler.summary()
@@ -691,6 +747,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="dmsgm", choices=["dmsgm", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--launch", default="graph", choices=["graph", "step"],
+                    help="timed steps as dmsgm_step_n graph replays (default) or single dmsgm_step launches (A/B)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -90,14 +90,23 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
  * coordinates to frame-(t-1) coordinates (R3), ignored for streams on their first
  * frame but always read; masks: u8 [S][height][mask_pitch] (device), written with
  * {0,255}.  Enqueued on `cuda_stream` (a cudaStream_t, NULL = legacy default stream);
- * returns after the enqueue (asynchronous).  Exactly one kernel launch. */
+ * returns after the enqueue (asynchronous).  Exactly one kernel launch.
+ * Stream ordering: the launch uses programmatic dependent launch (it may start while the
+ * previous kernel on `cuda_stream` drains), but every global-memory read of the step --
+ * frames, homographies, state -- follows griddepcontrol.wait, so inputs written by ANY
+ * earlier work on `cuda_stream` (a copy, a producer kernel, the previous step) are seen
+ * exactly as with plain stream order. */
 int dmsgm_step(dmsgm_ctx* ctx, const uint8_t* frames, size_t frame_pitch,
                const double* homographies, uint8_t* masks, size_t mask_pitch, void* cuda_stream);
 
 /* T consecutive frames per stream: frames u8 [T][S][height][frame_pitch], homographies
  * f64 [T][S][9], masks u8 [T][S][height][mask_pitch] (device).  The T launches are
  * captured once into a CUDA graph (re-captured when T or a pointer/pitch changes) and
- * replayed on `cuda_stream`.  Asynchronous. */
+ * replayed on `cuda_stream`.  Asynchronous.  The graph as a whole is ordered after earlier
+ * work on `cuda_stream`; inside it, step t+1's producer loads its first frame tile before
+ * waiting for step t (the frames of all T steps are inputs of the graph, so nothing inside
+ * it writes them) -- unless preprocessing or frame warping is on, whose kernels write the
+ * frames the step reads.  The frames, homographies and masks must not alias. */
 int dmsgm_step_n(dmsgm_ctx* ctx, int T, const uint8_t* frames, size_t frame_pitch,
                  const double* homographies, uint8_t* masks, size_t mask_pitch, void* cuda_stream);
 
@@ -106,7 +115,8 @@ int dmsgm_step_n(dmsgm_ctx* ctx, int T, const uint8_t* frames, size_t frame_pitc
  * written to host memory.  Streams are split into chunks whose H2D copy, kernel and
  * D2H copy are pipelined over internal CUDA streams ordered after `cuda_stream`.
  * SYNCHRONOUS: returns when the masks are in host memory.  Device staging buffers are
- * allocated on the first call and kept until dmsgm_destroy. */
+ * allocated on the first call, grown when the images get taller (dmsgm_set_band), and
+ * kept until dmsgm_destroy. */
 int dmsgm_step_host(dmsgm_ctx* ctx, const uint8_t* host_frames, size_t frame_pitch,
                     const double* host_homographies, uint8_t* host_masks, size_t mask_pitch,
                     void* cuda_stream);
@@ -114,9 +124,11 @@ int dmsgm_step_host(dmsgm_ctx* ctx, const uint8_t* host_frames, size_t frame_pit
 /* The same, ASYNCHRONOUS: returns after enqueueing.  Consecutive async calls pipeline
  * (step t+1's uploads overlap step t's kernels and downloads; each chunk of streams
  * follows its own previous chunk); work enqueued later on `cuda_stream`, and a sync of
- * it, sees the step complete.  It does NOT wait for earlier work on `cuda_stream` (its
- * inputs are host memory).  host_frames / host_homographies must stay unchanged and
- * host_masks unread until then. */
+ * it, sees the step complete.  It is ordered after this context's earlier dmsgm_step /
+ * dmsgm_step_n calls (it reads the state they write) and, on the context's first host
+ * step, after all earlier work on `cuda_stream`; it does NOT wait for other earlier work
+ * on `cuda_stream` (its inputs are host memory).  host_frames / host_homographies must
+ * stay unchanged and host_masks unread until then. */
 int dmsgm_step_host_async(dmsgm_ctx* ctx, const uint8_t* host_frames, size_t frame_pitch,
                           const double* host_homographies, uint8_t* host_masks, size_t mask_pitch,
                           void* cuda_stream);

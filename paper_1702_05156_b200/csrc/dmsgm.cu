@@ -55,6 +55,9 @@ struct dmsgm_ctx {
     uint8_t* st_frames;
     uint8_t* st_masks;
     double* st_H;
+    size_t st_bytes;   // capacity of st_frames / st_masks (a later dmsgm_set_band may need more)
+    cudaEvent_t ev_dev;   // recorded after device-side steps once step_host is in use
+    bool dev_pending;     // a device-side step was enqueued since the last step_host call
     cudaStream_t pipe[kPipeStreams];
     cudaEvent_t ev_start;
     cudaEvent_t ev_done[kPipeStreams];   // dmsgm_step_host_async: end of each pipe stream's work
@@ -136,8 +139,9 @@ bool encode_state_map(const dmsgm_ctx* c, float* base, int xc, int wrows, CUtens
 // Persistent TMA-staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
 template <int N, int BPT, int MINB, bool RULES, bool BAND = false>
 cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames, size_t fpitch, int s0,
-                          int count, int parity, int slot, cudaStream_t stream) {
+                          int count, int parity, int slot, cudaStream_t stream, bool early_frames) {
     StagedArgs sa;
+    sa.early_frames = early_frames ? 1 : 0;
     sa.tiles_xc = (c->Wb + Staged<N, BPT>::TWB - 1) / Staged<N, BPT>::TWB;
     sa.tiles_y = (c->rows + kCtaY - 1) / kCtaY;
     sa.items = count * sa.tiles_xc * sa.tiles_y;
@@ -355,10 +359,13 @@ void launch_kernel(const StepArgs& a, dim3 grid, dim3 block, cudaStream_t stream
     dmsgm_step_kernel<N, BPT><<<grid, block, 0, stream>>>(a);
 }
 
-// Enqueue one kernel for streams [s0, s0+count) of the batch.
+// Enqueue one kernel for streams [s0, s0+count) of the batch.  early_frames: the kernel
+// preceding this launch on `stream` cannot have written `frames` (StagedArgs::early_frames;
+// ignored, i.e. off, when a filter / warp kernel of this context produces the frames).
 cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, const double* H,
                         uint8_t* masks, size_t mpitch, int s0, int count, int parity,
-                        cudaStream_t stream, int slot = 0) {
+                        cudaStream_t stream, int slot = 0, bool early_frames = false) {
+    if (c->pf_buf || c->wf_buf) early_frames = false;
     if (c->pf_buf) {
         // preprocessing (R34): the filtered frames replace the frames for the whole step
         uint8_t* pf = c->pf_buf + (size_t)s0 * c->Hp * c->pf_pitch;
@@ -417,8 +424,10 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
         // otherwise the default rules are compiled in without branches.
         const bool rules = c->p.update_rule != 0 || c->p.classify_rule != 0;
 #define DMSGM_BAND(NN, BB)                                                                                    \
-    return rules ? launch_staged<NN, BB, 3, true, true>(c, a, frames, fpitch, s0, count, parity, slot, stream) \
-                 : launch_staged<NN, BB, 3, false, true>(c, a, frames, fpitch, s0, count, parity, slot, stream)
+    return rules ? launch_staged<NN, BB, 3, true, true>(c, a, frames, fpitch, s0, count, parity, slot, stream,   \
+                                                        early_frames)                                          \
+                 : launch_staged<NN, BB, 3, false, true>(c, a, frames, fpitch, s0, count, parity, slot, stream,  \
+                                                         early_frames)
         if (c->band) {   // band mode: halo check + neighbour stores compiled in
             if (c->N == 1) { DMSGM_BAND(1, 2); }
             if (c->N == 2) { DMSGM_BAND(2, 2); }
@@ -427,8 +436,10 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
         }
 #undef DMSGM_BAND
 #define DMSGM_STAGED(NN, BB, OO)                                                                            \
-    return rules ? launch_staged<NN, BB, OO, true>(c, a, frames, fpitch, s0, count, parity, slot, stream)    \
-                 : launch_staged<NN, BB, OO, false>(c, a, frames, fpitch, s0, count, parity, slot, stream)
+    return rules ? launch_staged<NN, BB, OO, true>(c, a, frames, fpitch, s0, count, parity, slot, stream,       \
+                                                   early_frames)                                               \
+                 : launch_staged<NN, BB, OO, false>(c, a, frames, fpitch, s0, count, parity, slot, stream,      \
+                                                    early_frames)
 #define DMSGM_STAGED_OCC(NN, BB)                      \
     if (c->staged_occ == 3) { DMSGM_STAGED(NN, BB, 3); } \
     DMSGM_STAGED(NN, BB, 4)
@@ -465,6 +476,16 @@ int check_images(dmsgm_ctx* c, const void* frames, size_t fpitch, const void* H,
 }
 
 bool has_peers(const dmsgm_ctx* c) { return c->peer_slot[0] || c->peer_slot[1]; }
+
+// Once dmsgm_step_host(_async) is in use, a device-side step records ev_dev so that a
+// following dmsgm_step_host_async orders its kernels after it (they read the state it wrote).
+int note_device_step(dmsgm_ctx* c, void* stream) {
+    if (!c->pipe_ready) return DMSGM_OK;     // the first step_host call waits on the whole stream
+    cudaError_t e = cudaEventRecord(c->ev_dev, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaEventRecord");
+    c->dev_pending = true;
+    return DMSGM_OK;
+}
 
 
 // Enqueue the band signal / wait kernel (one thread).
@@ -593,6 +614,7 @@ int dmsgm_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, const double*
     cudaError_t e = launch_step(c, frames, fpitch, H, masks, mpitch, 0, c->S, c->cur,
                                 (cudaStream_t)cuda_stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_step launch");
+    if ((rc = note_device_step(c, cuda_stream))) return rc;
     c->cur ^= 1;
     c->steps += 1;
     return DMSGM_OK;
@@ -625,8 +647,11 @@ int dmsgm_step_n(dmsgm_ctx* c, int T, const uint8_t* frames, size_t fpitch, cons
         int parity = c->cur;
         cudaError_t le = cudaSuccess;
         for (int t = 0; t < T && le == cudaSuccess; ++t) {
+            // the frames are graph inputs (written before the graph is launched) and the
+            // node before each step is the previous step or band-sync kernel: the producer
+            // may load its first frame box before griddepcontrol.wait
             le = launch_step(c, frames + t * fframe, fpitch, H + (size_t)t * c->S * 9, masks + t * mframe,
-                             mpitch, 0, c->S, parity, c->capture_stream);
+                             mpitch, 0, c->S, parity, c->capture_stream, 0, true);
             // band mode with neighbours: every step ends with the signal / wait exchange
             if (le == cudaSuccess && has_peers(c)) le = launch_sync(c, 1, 1, c->capture_stream);
             parity ^= 1;
@@ -643,6 +668,7 @@ int dmsgm_step_n(dmsgm_ctx* c, int T, const uint8_t* frames, size_t fpitch, cons
     }
     e = cudaGraphLaunch(slot->exec, (cudaStream_t)cuda_stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphLaunch");
+    if ((rc = note_device_step(c, cuda_stream))) return rc;
     if (T & 1) c->cur ^= 1;
     c->steps += (unsigned)T;
     return DMSGM_OK;
@@ -662,29 +688,59 @@ int step_host_impl(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double*
     const size_t fimg = (size_t)c->Hp * dpitch;
     int rc = check_status(c);
     if (rc) return rc;
+    bool first = false;
     if (!c->pipe_ready) {
-        const size_t nb = (size_t)c->S * fimg;
-        if ((e = cudaMalloc(&c->st_frames, nb)) != cudaSuccess || (e = cudaMalloc(&c->st_masks, nb)) != cudaSuccess ||
-            (e = cudaMalloc(&c->st_H, (size_t)c->S * 9 * sizeof(double))) != cudaSuccess)
-            return fail(c, DMSGM_ENOMEM, "staging cudaMalloc failed: %s", cudaGetErrorString(e));
         for (int i = 0; i < kPipeStreams; ++i)
             if ((e = cudaStreamCreateWithFlags(&c->pipe[i], cudaStreamNonBlocking)) != cudaSuccess)
                 return cuda_fail(c, e, "cudaStreamCreate");
-        if ((e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming)) != cudaSuccess)
+        if ((e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&c->ev_dev, cudaEventDisableTiming)) != cudaSuccess)
             return cuda_fail(c, e, "cudaEventCreate");
         for (int i = 0; i < kPipeStreams; ++i)
             if ((e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming)) != cudaSuccess)
                 return cuda_fail(c, e, "cudaEventCreate");
         c->pipe_ready = true;
+        first = true;
     }
-    if (!async) {
+    const size_t nb = (size_t)c->S * fimg;
+    if (nb > c->st_bytes) {
+        // (re)allocate: the first call, or a band / whole-frame switch that made images taller;
+        // earlier async steps may still read / write the old buffers
+        for (int i = 0; i < kPipeStreams; ++i)
+            if ((e = cudaStreamSynchronize(c->pipe[i])) != cudaSuccess) return cuda_fail(c, e, "staging sync");
+        if (c->st_frames) cudaFree(c->st_frames);
+        if (c->st_masks) cudaFree(c->st_masks);
+        c->st_frames = nullptr;
+        c->st_masks = nullptr;
+        c->st_bytes = 0;
+        if ((e = cudaMalloc(&c->st_frames, nb)) != cudaSuccess || (e = cudaMalloc(&c->st_masks, nb)) != cudaSuccess) {
+            if (c->st_frames) cudaFree(c->st_frames);
+            c->st_frames = nullptr;
+            c->st_masks = nullptr;
+            return fail(c, DMSGM_ENOMEM, "staging cudaMalloc failed: %s", cudaGetErrorString(e));
+        }
+        c->st_bytes = nb;
+    }
+    if (!c->st_H && (e = cudaMalloc(&c->st_H, (size_t)c->S * 9 * sizeof(double))) != cudaSuccess) {
+        c->st_H = nullptr;
+        return fail(c, DMSGM_ENOMEM, "staging cudaMalloc failed: %s", cudaGetErrorString(e));
+    }
+    if (!async || first) {
         // ordered after the caller's earlier work on cuda_stream
         if ((e = cudaEventRecord(c->ev_start, (cudaStream_t)cuda_stream)) != cudaSuccess)
             return cuda_fail(c, e, "cudaEventRecord");
         for (int i = 0; i < kPipeStreams; ++i)
             if ((e = cudaStreamWaitEvent(c->pipe[i], c->ev_start, 0)) != cudaSuccess)
                 return cuda_fail(c, e, "cudaStreamWaitEvent");
+    } else if (c->dev_pending) {
+        // an async step after device-side steps: its kernels read the state those wrote
+        // (waiting on the last one, not on all of cuda_stream, keeps consecutive async
+        // steps pipelined)
+        for (int i = 0; i < kPipeStreams; ++i)
+            if ((e = cudaStreamWaitEvent(c->pipe[i], c->ev_dev, 0)) != cudaSuccess)
+                return cuda_fail(c, e, "cudaStreamWaitEvent");
     }
+    c->dev_pending = false;
     // chunks of streams: H2D(k) || kernel(k-1) || D2H(k-2) across the pipe streams
     const char* cenv = getenv("DMSGM_HOST_CHUNKS");
     int nchunks = cenv ? atoi(cenv) : 8;
@@ -1158,6 +1214,7 @@ void dmsgm_destroy(dmsgm_ctx* c) {
             cudaEventDestroy(c->ev_done[i]);
         }
         cudaEventDestroy(c->ev_start);
+        cudaEventDestroy(c->ev_dev);
     }
     if (c->st_frames) cudaFree(c->st_frames);
     if (c->st_masks) cudaFree(c->st_masks);

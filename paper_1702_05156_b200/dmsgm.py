@@ -158,6 +158,58 @@ def _row_pitch(t) -> int:
     return t.stride(-2) * t.element_size()
 
 
+def _strides_bytes(t):
+    if isinstance(t, np.ndarray):
+        return tuple(t.strides), t.dtype.itemsize
+    return tuple(st * t.element_size() for st in t.stride()), t.element_size()
+
+
+def _dtype_name(t) -> str:
+    return str(t.dtype).replace("torch.", "")
+
+
+def _check_tensor(name, t, shape, dtype, device, pitch_rows=None):
+    """Argument marshalling guard for the C ABI: the library reads raw pointers with the
+    [..][rows][pitch] / [..][9] layouts include/dmsgm.h states, so dtype, shape, device and
+    the outer strides are checked here (ValueError) before a pointer is passed.  Raw
+    integer pointers are passed through unchecked."""
+    if isinstance(t, int):
+        return
+    if _dtype_name(t) != dtype:
+        raise ValueError(f"{name}: dtype {_dtype_name(t)}, expected {dtype}")
+    ok = tuple(t.shape) == tuple(shape)
+    if pitch_rows is not None:                   # images: the last dim may be a padded pitch >= width
+        ok = tuple(t.shape[:-1]) == tuple(shape[:-1]) and t.shape[-1] >= shape[-1]
+    if not ok:
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}"
+                         f"{' (last dim >= width)' if pitch_rows is not None else ''}")
+    if device == "cpu":
+        if not isinstance(t, np.ndarray) and t.is_cuda:
+            raise ValueError(f"{name}: expected host memory, got a CUDA tensor")
+    else:
+        if isinstance(t, np.ndarray) or not t.is_cuda:
+            raise ValueError(f"{name}: expected a CUDA tensor on device {device}")
+        if t.device.index != device:
+            raise ValueError(f"{name}: on cuda:{t.device.index}, the context is on cuda:{device}")
+    st, es = _strides_bytes(t)
+    if st[-1] != es:
+        raise ValueError(f"{name}: the last dimension must be contiguous")
+    if pitch_rows is None:                      # homographies: dense [..][9] f64
+        expect = es
+        for d in range(len(shape) - 1, -1, -1):
+            if shape[d] > 1 and st[d] != expect:
+                raise ValueError(f"{name}: must be contiguous")
+            expect *= shape[d]
+        return
+    pitch = st[-2]                               # images: [..][rows][pitch] per image, images dense
+    expect = pitch * pitch_rows
+    for d in range(len(shape) - 3, -1, -1):
+        if shape[d] > 1 and st[d] != expect:
+            raise ValueError(f"{name}: dimension {d} stride {st[d]} B, expected {expect} B "
+                             f"(images of {pitch_rows} rows x {pitch} B must be consecutive)")
+        expect *= shape[d]
+
+
 class Dmsgm:
     """Python view of one dmsgm_ctx.  Names follow include/dmsgm.h."""
 
@@ -171,9 +223,17 @@ class Dmsgm:
         if rc != DMSGM_OK:
             raise DmsgmError(rc, self._lib.dmsgm_last_error(None).decode())
         self._h = h
+        self.device = device
         self.info = self.get_info()
 
     # -- helpers -------------------------------------------------------------
+    def _check_args(self, frames, homographies, masks, lead, device):
+        rows = self.info.band_rows * self.block            # pixel rows of a (band) image
+        S = self.info.num_streams
+        _check_tensor("frames", frames, (*lead, S, rows, self.width), "uint8", device, rows)
+        _check_tensor("masks", masks, (*lead, S, rows, self.width), "uint8", device, rows)
+        _check_tensor("homographies", homographies, (*lead, S, 9), "float64", device)
+
     def _check(self, rc: int):
         if rc < 0:
             raise DmsgmError(rc, self._lib.dmsgm_last_error(self._h).decode())
@@ -197,21 +257,25 @@ class Dmsgm:
     # -- C ABI ---------------------------------------------------------------
     def step(self, frames, homographies, masks, stream=None):
         """frames/masks: uint8 CUDA [S][H][W] (row pitch from strides); homographies f64 [S][9]."""
+        self._check_args(frames, homographies, masks, (), self.device)
         self._check(self._lib.dmsgm_step(self._h, _ptr(frames), _row_pitch(frames), _ptr(homographies),
                                          _ptr(masks), _row_pitch(masks), _stream_handle(stream)))
 
     def step_n(self, T: int, frames, homographies, masks, stream=None):
         """frames/masks: uint8 CUDA [T][S][H][W]; homographies f64 [T][S][9]."""
+        self._check_args(frames, homographies, masks, (T,), self.device)
         self._check(self._lib.dmsgm_step_n(self._h, T, _ptr(frames), _row_pitch(frames), _ptr(homographies),
                                            _ptr(masks), _row_pitch(masks), _stream_handle(stream)))
 
     def step_host(self, frames, homographies, masks, stream=None):
         """HOST buffers (numpy or pinned CPU tensors); synchronous."""
+        self._check_args(frames, homographies, masks, (), "cpu")
         self._check(self._lib.dmsgm_step_host(self._h, _ptr(frames), _row_pitch(frames), _ptr(homographies),
                                               _ptr(masks), _row_pitch(masks), _stream_handle(stream)))
 
     def step_host_async(self, frames, homographies, masks, stream=None):
         """HOST buffers (pinned); returns after enqueueing (see include/dmsgm.h)."""
+        self._check_args(frames, homographies, masks, (), "cpu")
         self._check(self._lib.dmsgm_step_host_async(self._h, _ptr(frames), _row_pitch(frames), _ptr(homographies),
                                                     _ptr(masks), _row_pitch(masks), _stream_handle(stream)))
 

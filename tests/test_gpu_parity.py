@@ -234,9 +234,24 @@ def test_argument_errors_gpu(cuda_lib):
     f = torch.zeros((1, 48, 64), dtype=torch.uint8, device="cuda")
     h = torch.zeros((1, 9), dtype=torch.float64, device="cuda")
     m = torch.zeros_like(f)
+    wide = torch.zeros((1, 48, 80), dtype=torch.uint8, device="cuda")
     with pytest.raises(dm.DmsgmError) as ei:
-        ctx.step(f[:, :, 1:], h, m)        # misaligned base pointer
+        ctx.step(wide[:, :, 1:65], h, m)   # misaligned base pointer (the C ABI's check)
     assert ei.value.code == dm.DMSGM_EINVAL
+    # the binding's marshalling checks: dtype, shape, device, outer strides
+    with pytest.raises(ValueError, match="dtype"):
+        ctx.step(f, h.float(), m)          # f32 homographies
+    with pytest.raises(ValueError, match="shape"):
+        ctx.step(f[:, :, 1:], h, m)
+    with pytest.raises(ValueError, match="CUDA"):
+        ctx.step(f.cpu(), h, m)
+    two = torch.zeros((2, 48, 64), dtype=torch.uint8, device="cuda")
+    ctx2 = dm.Dmsgm(64, 48, 4, dm.Params(num_streams=2))
+    with pytest.raises(ValueError, match="stride"):
+        ctx2.step(torch.zeros((48, 2, 64), dtype=torch.uint8, device="cuda").transpose(0, 1), h.repeat(2, 1), two)
+    with pytest.raises(ValueError, match="host"):
+        ctx2.step_host(two, h.repeat(2, 1).cpu(), two.cpu())
+    ctx2.close()
     bad = np.zeros((6, 12, 16), np.float32)
     bad[0, 0, 0] = np.nan
     with pytest.raises(dm.DmsgmError):
