@@ -13,9 +13,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB_PATH = os.path.join(PKG, "libdmsgm.so")
-SOURCES = [os.path.join(CSRC, "dmsgm.cu")]
+SOURCES = [os.path.join(CSRC, "dmsgm.cu"), os.path.join(CSRC, "dmsgm_klt.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
-    [os.path.join(INCLUDE, "dmsgm.h")]
+    [os.path.join(INCLUDE, "dmsgm.h"), os.path.join(INCLUDE, "dmsgm_klt.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

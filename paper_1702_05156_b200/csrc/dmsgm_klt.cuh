@@ -1,0 +1,803 @@
+// dmsgm_klt.cuh -- sm_100a kernels of the motion estimation that feeds the DMSGM step its
+// homographies (App. F: goodFeaturesToTrack ->
+// calcOpticalFlowPyrLK(Size(20,20), 5) -> findHomography(CV_RANSAC)).  Readings R38-R42
+// (include/dmsgm_klt.h).  One launch of each kernel covers every stream of
+// the batch:
+//   klt_score_kernel    exact Sobel/structure tensor, fp64 lambda_min, 3x3 local maxima
+//                       appended as 64-bit keys (score bits | ~raster index), per-stream
+//                       max score (R38)
+//   klt_select_kernel   one CTA per stream: exact top-2048 of the qualifying keys by an
+//                       8-pass radix select, bitonic sort in shared memory, greedy
+//                       min-distance selection by one warp over a cell grid (R38)
+//   klt_pyramid_kernel  all box-pyramid levels of prev and next in one pass (R39)
+//   klt_lk_kernel       one warp per corner, pyramidal Lucas-Kanade in fp32 (R40)
+//   klt_compact_kernel  tracked pairs -> RANSAC matches (f64), one warp per stream
+//   klt_ransac_kernel   one warp per (stream, iteration): SplitMix64 sample, 8x8 fp64
+//                       solve, inlier count (R42)
+//   klt_refit_kernel    one warp per stream: best model, its inliers, normalized DLT by
+//                       the smallest eigenvector of A^T A (cyclic Jacobi, fp64) (R41)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dmsgm_klt {
+
+constexpr int kMaxLevels = 6;        // levels 0..5
+constexpr int kMaxCorners = 1024;
+constexpr int kBatch = 2048;         // keys per greedy batch (radix-selected, then sorted)
+constexpr int kSelThreads = 1024;
+constexpr int kTX = 32, kTY = 8;     // score tile
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// ---------------------------------------------------------------------------------------
+// K1: Shi-Tomasi score (R38) + 3x3 local maxima -> candidate keys, per-stream max score
+// ---------------------------------------------------------------------------------------
+struct ScoreArgs {
+    const uint8_t* frames;
+    long long fstride;
+    int pitch, W, H;
+    unsigned long long* cand;   // [S][cap]
+    int cap;
+    unsigned* count;            // [S]
+    unsigned* maxbits;          // [S] float bits of the max score (scores are >= +0)
+};
+
+__global__ void __launch_bounds__(256) klt_score_kernel(const ScoreArgs a) {
+    const int s = blockIdx.z;
+    const uint8_t* f = a.frames + (long long)s * a.fstride;
+    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+    const int W = a.W, H = a.H, pitch = a.pitch;
+    // gradients at (clamp(x0-2+i), clamp(y0-2+j)): the replicated-border gradient products
+    // of the structure-tensor window (the oracle pads the products, not the pixels)
+    __shared__ int gxs[kTY + 4][kTX + 4];
+    __shared__ int gys[kTY + 4][kTX + 4];
+    __shared__ float sc[kTY + 2][kTX + 2];
+    __shared__ float wmax[8];
+    const int tid = threadIdx.x;
+    for (int k = tid; k < (kTY + 4) * (kTX + 4); k += 256) {
+        const int j = k / (kTX + 4), i = k - j * (kTX + 4);
+        const int X = clampi(x0 - 2 + i, 0, W - 1), Y = clampi(y0 - 2 + j, 0, H - 1);
+        const int xm = X > 0 ? X - 1 : 0, xp = X < W - 1 ? X + 1 : W - 1;
+        const int ym = Y > 0 ? Y - 1 : 0, yp = Y < H - 1 ? Y + 1 : H - 1;
+        const uint8_t* rm = f + (long long)ym * pitch;
+        const uint8_t* r0 = f + (long long)Y * pitch;
+        const uint8_t* rp = f + (long long)yp * pitch;
+        const int mm = __ldg(rm + xm), m0 = __ldg(rm + X), mp = __ldg(rm + xp);
+        const int zm = __ldg(r0 + xm), zp = __ldg(r0 + xp);
+        const int pm = __ldg(rp + xm), p0 = __ldg(rp + X), pp = __ldg(rp + xp);
+        gxs[j][i] = (mp + 2 * zp + pp) - (mm + 2 * zm + pm);
+        gys[j][i] = (pm + 2 * p0 + pp) - (mm + 2 * m0 + mp);
+    }
+    __syncthreads();
+    for (int k = tid; k < (kTY + 2) * (kTX + 2); k += 256) {
+        const int j = k / (kTX + 2), i = k - j * (kTX + 2);
+        const int X = x0 - 1 + i, Y = y0 - 1 + j;
+        float v = -1.0f;                              // outside the frame: never compared
+        if (X >= 0 && X < W && Y >= 0 && Y < H) {
+            int sa = 0, sb = 0, scc = 0;
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
+                    const int gx = gxs[j + dy][i + dx], gy = gys[j + dy][i + dx];
+                    sa += gx * gx;
+                    sb += gx * gy;
+                    scc += gy * gy;
+                }
+            const long long d = (long long)(sa - scc) * (long long)(sa - scc) + 4LL * (long long)sb * (long long)sb;
+            const double lam = __dmul_rn(__dsub_rn((double)(sa + scc), __dsqrt_rn((double)d)), 0.5);
+            v = __double2float_rn(lam);
+        }
+        sc[j][i] = v;
+    }
+    __syncthreads();
+    const int tx = tid & 31, ty = tid >> 5;
+    const int x = x0 + tx, y = y0 + ty;
+    const bool in = x < W && y < H;
+    const float v = in ? sc[ty + 1][tx + 1] : 0.0f;
+    bool cand = in && x >= 1 && x < W - 1 && y >= 1 && y < H - 1 && v > 0.0f;
+    if (cand) {
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) cand &= v >= sc[ty + dy][tx + dx];
+    }
+    // block max of the score over every pixel of the frame (the oracle's score.max())
+    float m = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tx == 0) wmax[ty] = m;
+    // candidates: warp-aggregated append
+    const unsigned bal = __ballot_sync(0xffffffffu, cand);
+    if (bal) {
+        unsigned base = 0;
+        if (tx == 0) base = atomicAdd(a.count + s, (unsigned)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (cand) {
+            const unsigned pos = base + __popc(bal & ((1u << tx) - 1u));
+            const unsigned idx = (unsigned)(y * W + x);
+            if (pos < (unsigned)a.cap)
+                a.cand[(long long)s * a.cap + pos] =
+                    ((unsigned long long)__float_as_uint(v) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        float bm = wmax[0];
+        for (int w = 1; w < 8; ++w) bm = fmaxf(bm, wmax[w]);
+        atomicMax(a.maxbits + s, __float_as_uint(bm));    // scores >= +0: bits order like values
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K2: quality threshold, exact top-kBatch radix select, bitonic sort, greedy min-distance
+// ---------------------------------------------------------------------------------------
+struct SelectArgs {
+    const unsigned long long* cand;
+    int cap;
+    const unsigned* count;
+    const unsigned* maxbits;
+    double quality, min_dist2;
+    int W, max_corners;
+    int cell, gw, gh;            // greedy cell grid: cell side (px), columns, rows
+    uint16_t* grid_global;       // [S][gh][gw] when the grid does not fit shared memory (else null)
+    int* corners_out;            // [S][max_corners][2]
+    int* counts_out;             // [S]
+    unsigned* overflow;          // set to 1 if a stream had more candidates than cap
+};
+
+__device__ __forceinline__ bool qualifies(unsigned long long k, double thr) {
+    return (double)__uint_as_float((unsigned)(k >> 32)) >= thr;
+}
+
+__global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    unsigned long long* batch = reinterpret_cast<unsigned long long*>(sm);      // [kBatch]
+    unsigned* hist = reinterpret_cast<unsigned*>(batch + kBatch);               // [256]
+    int* kept = reinterpret_cast<int*>(hist + 256);                             // [kMaxCorners][2]
+    uint16_t* grid_s = reinterpret_cast<uint16_t*>(kept + 2 * kMaxCorners);
+    __shared__ unsigned long long s_prefix, s_mask;
+    __shared__ unsigned s_rem, s_total, s_m;
+    __shared__ int s_nkept, s_done;
+    const int s = blockIdx.x, tid = threadIdx.x;
+    const unsigned cnt = a.count[s];
+    if (tid == 0 && cnt > (unsigned)a.cap) *a.overflow = 1u;
+    const int n = cnt < (unsigned)a.cap ? (int)cnt : a.cap;
+    const unsigned long long* cand = a.cand + (long long)s * a.cap;
+    const float mx = __uint_as_float(a.maxbits[s]);
+    const double thr = a.quality * (double)mx;
+    uint16_t* grid = a.grid_global ? a.grid_global + (long long)s * a.gw * a.gh : grid_s;
+    const int ncell = a.gw * a.gh;
+    for (int i = tid; i < ncell; i += kSelThreads) grid[i] = 0;
+    if (tid == 0) { s_nkept = 0; s_done = !(mx > 0.0f) || a.max_corners == 0; }
+    __syncthreads();
+    unsigned long long upper = ~0ull;             // this batch: keys below `upper`
+    while (!s_done) {
+        // ---- exact radix select of the kBatch-th largest qualifying key below `upper` ----
+        if (tid == 0) { s_prefix = 0; s_mask = 0; s_rem = kBatch; }
+        unsigned long long cut = 0;
+        bool all = false;
+        for (int pass = 0; pass < 8; ++pass) {
+            const int shift = 56 - 8 * pass;
+            if (tid < 256) hist[tid] = 0;
+            __syncthreads();
+            const unsigned long long pre = s_prefix, msk = s_mask;
+            for (int i = tid; i < n; i += kSelThreads) {
+                const unsigned long long k = cand[i];
+                if (k < upper && (k & msk) == pre && qualifies(k, thr)) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                if (pass == 0) {
+                    unsigned t = 0;
+                    for (int d = 0; d < 256; ++d) t += hist[d];
+                    s_total = t;
+                }
+                if (pass > 0 || s_total > (unsigned)kBatch) {
+                    unsigned cum = 0, rem = s_rem;
+                    int d = 255;
+                    for (; d > 0; --d) {
+                        if (cum + hist[d] >= rem) break;
+                        cum += hist[d];
+                    }
+                    s_rem = rem - cum;
+                    s_prefix |= (unsigned long long)d << shift;
+                    s_mask |= 0xFFull << shift;
+                }
+            }
+            __syncthreads();
+            if (s_total <= (unsigned)kBatch) { all = true; break; }
+        }
+        if (!all) cut = s_prefix;                 // the kBatch-th largest key (keys are unique)
+        // ---- gather the batch: qualifying keys in [cut, upper) ----
+        if (tid == 0) s_m = 0;
+        __syncthreads();
+        for (int i = tid; i < n; i += kSelThreads) {
+            const unsigned long long k = cand[i];
+            if (k < upper && k >= cut && qualifies(k, thr)) batch[atomicAdd(&s_m, 1u)] = k;
+        }
+        __syncthreads();
+        const int m = (int)s_m;
+        int P = 1;
+        while (P < m) P <<= 1;
+        for (int i = m + tid; i < P; i += kSelThreads) batch[i] = 0ull;
+        __syncthreads();
+        // ---- bitonic sort, descending ----
+        for (int size = 2; size <= P; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = tid; i < P; i += kSelThreads) {
+                    const int j = i ^ stride;
+                    if (j > i) {
+                        const unsigned long long u = batch[i], w = batch[j];
+                        const bool desc = (i & size) == 0;
+                        if (desc ? (u < w) : (u > w)) { batch[i] = w; batch[j] = u; }
+                    }
+                }
+                __syncthreads();
+            }
+        // ---- greedy selection by warp 0: a cell holds at most one kept corner ----
+        if (tid < 32) {
+            const int lane = tid;
+            int nk = s_nkept;
+            const int dx = lane % 5 - 2, dy = lane / 5 - 2;
+            for (int j = 0; j < m && nk < a.max_corners; ++j) {
+                const unsigned idx = 0xFFFFFFFFu - (unsigned)batch[j];
+                const int y = (int)(idx / (unsigned)a.W), x = (int)(idx - (unsigned)y * (unsigned)a.W);
+                const int cx = x / a.cell, cy = y / a.cell;
+                bool conflict = false;
+                if (lane < 25) {
+                    const int gx = cx + dx, gy = cy + dy;
+                    if (gx >= 0 && gx < a.gw && gy >= 0 && gy < a.gh) {
+                        const int e = *(volatile uint16_t*)(grid + gy * a.gw + gx);
+                        if (e) {
+                            const int kx = kept[2 * (e - 1)], ky = kept[2 * (e - 1) + 1];
+                            const int ddx = x - kx, ddy = y - ky;
+                            conflict = (double)(ddx * ddx + ddy * ddy) < a.min_dist2;
+                        }
+                    }
+                }
+                if (!__any_sync(0xffffffffu, conflict)) {
+                    if (lane == 0) {
+                        kept[2 * nk] = x;
+                        kept[2 * nk + 1] = y;
+                        *(volatile uint16_t*)(grid + cy * a.gw + cx) = (uint16_t)(nk + 1);
+                        a.corners_out[((long long)s * a.max_corners + nk) * 2] = x;
+                        a.corners_out[((long long)s * a.max_corners + nk) * 2 + 1] = y;
+                    }
+                    ++nk;
+                    __syncwarp();
+                }
+            }
+            if (lane == 0) {
+                s_nkept = nk;
+                s_done = nk >= a.max_corners || all;
+            }
+        }
+        __syncthreads();
+        upper = cut;
+    }
+    if (tid == 0) a.counts_out[s] = s_nkept;
+}
+
+// ---------------------------------------------------------------------------------------
+// K3: box pyramid levels 1..nlev-1 of prev (set 0) and next (set 1) in one pass (R39)
+// ---------------------------------------------------------------------------------------
+struct PyrArgs {
+    const uint8_t* img0[2];
+    long long stride0[2];
+    int pitch0[2];
+    uint8_t* lev[kMaxLevels];      // level L >= 1: [2][S][h_L][w_L]
+    int w[kMaxLevels], h[kMaxLevels];
+    int nlev, S;
+};
+
+__global__ void __launch_bounds__(256) klt_pyramid_kernel(const PyrArgs a) {
+    __shared__ int t[2][16][16];
+    const int z = blockIdx.z, set = z / a.S, s = z - set * a.S;
+    const uint8_t* src = a.img0[set] + (long long)s * a.stride0[set];
+    const int p0 = a.pitch0[set];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    int cur = 0;
+    {
+        const int x = blockIdx.x * 16 + tx, y = blockIdx.y * 16 + ty;
+        int v = 0;
+        if (x < a.w[1] && y < a.h[1]) {
+            const uint8_t* r0 = src + (long long)(2 * y) * p0 + 2 * x;
+            v = (r0[0] + r0[1] + r0[p0] + r0[p0 + 1] + 2) >> 2;
+            a.lev[1][((long long)z * a.h[1] + y) * a.w[1] + x] = (uint8_t)v;
+        }
+        t[0][ty][tx] = v;
+    }
+    for (int L = 2; L < a.nlev; ++L) {
+        __syncthreads();
+        const int side = 16 >> (L - 1);
+        if (tx < side && ty < side) {
+            const int x = blockIdx.x * side + tx, y = blockIdx.y * side + ty;
+            const int v = (t[cur][2 * ty][2 * tx] + t[cur][2 * ty][2 * tx + 1] + t[cur][2 * ty + 1][2 * tx] +
+                           t[cur][2 * ty + 1][2 * tx + 1] + 2) >> 2;
+            if (x < a.w[L] && y < a.h[L]) a.lev[L][((long long)z * a.h[L] + y) * a.w[L] + x] = (uint8_t)v;
+            t[cur ^ 1][ty][tx] = v;
+        }
+        cur ^= 1;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K4: pyramidal Lucas-Kanade, one warp per corner (R40)
+// ---------------------------------------------------------------------------------------
+struct Img {
+    const uint8_t* p;
+    long long stride;   // bytes between streams
+    int pitch, w, h;
+};
+
+struct LkArgs {
+    Img prev[kMaxLevels], next[kMaxLevels];
+    int nlev, win, max_iters, max_corners;
+    float eps2, min_eig;
+    const int* corners;     // [S][max_corners][2]
+    const int* counts;      // [S]
+    float* tracked;         // [S][max_corners][2]
+    uint8_t* status;        // [S][max_corners]
+};
+
+// bilinear value at continuous coordinates (pixel centres at +0.5), border pixels repeated
+__device__ __forceinline__ float bil(const uint8_t* img, int pitch, int w, int h, float cx, float cy) {
+    const float ux = __fsub_rn(cx, 0.5f), uy = __fsub_rn(cy, 0.5f);
+    const float xf = floorf(ux), yf = floorf(uy);
+    const float fx = __fsub_rn(ux, xf), fy = __fsub_rn(uy, yf);
+    const int x0 = (int)xf, y0 = (int)yf;
+    const int xa = clampi(x0, 0, w - 1), xb = clampi(x0 + 1, 0, w - 1);
+    const int ya = clampi(y0, 0, h - 1), yb = clampi(y0 + 1, 0, h - 1);
+    const uint8_t* ra = img + (long long)ya * pitch;
+    const uint8_t* rb = img + (long long)yb * pitch;
+    const float gx = __fsub_rn(1.0f, fx);
+    const float top = __fadd_rn(__fmul_rn((float)__ldg(ra + xa), gx), __fmul_rn((float)__ldg(ra + xb), fx));
+    const float bot = __fadd_rn(__fmul_rn((float)__ldg(rb + xa), gx), __fmul_rn((float)__ldg(rb + xb), fx));
+    return __fadd_rn(__fmul_rn(top, __fsub_rn(1.0f, fy)), __fmul_rn(bot, fy));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int NS>   // samples per lane: ceil(win^2 / 32)
+__global__ void __launch_bounds__(256) klt_lk_kernel(const LkArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int s = blockIdx.y;
+    if (i >= a.max_corners) return;
+    const long long o = (long long)s * a.max_corners + i;
+    if (i >= a.counts[s]) {
+        if (lane == 0) {
+            a.status[o] = 0;
+            a.tracked[2 * o] = __int_as_float(0x7fc00000);
+            a.tracked[2 * o + 1] = __int_as_float(0x7fc00000);
+        }
+        return;
+    }
+    const float cx = (float)a.corners[2 * o] + 0.5f, cy = (float)a.corners[2 * o + 1] + 0.5f;
+    const int win = a.win, nsamp = win * win;
+    const float half = 0.5f * (float)(win - 1);
+    float gx = 0.0f, gy = 0.0f;
+    bool ok = true;
+    for (int L = a.nlev - 1; L >= 0 && ok; --L) {
+        const Img P = a.prev[L], Q = a.next[L];
+        const uint8_t* pp = P.p + (long long)s * P.stride;
+        const uint8_t* qp = Q.p + (long long)s * Q.stride;
+        const float sc = __int_as_float((127 - L) << 23);        // 2^-L
+        const float plx = __fmul_rn(cx, sc), ply = __fmul_rn(cy, sc);
+        float I[NS], Ix[NS], Iy[NS], sx[NS], sy[NS];
+        float gxx = 0.0f, gxy = 0.0f, gyy = 0.0f;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const int q = lane + 32 * k;
+            I[k] = Ix[k] = Iy[k] = 0.0f;
+            sx[k] = sy[k] = 0.0f;
+            if (q < nsamp) {
+                const int jj = q / win, ii = q - jj * win;
+                sx[k] = __fadd_rn(plx, __fsub_rn((float)ii, half));
+                sy[k] = __fadd_rn(ply, __fsub_rn((float)jj, half));
+                I[k] = bil(pp, P.pitch, P.w, P.h, sx[k], sy[k]);
+                Ix[k] = __fmul_rn(__fsub_rn(bil(pp, P.pitch, P.w, P.h, __fadd_rn(sx[k], 1.0f), sy[k]),
+                                            bil(pp, P.pitch, P.w, P.h, __fsub_rn(sx[k], 1.0f), sy[k])), 0.5f);
+                Iy[k] = __fmul_rn(__fsub_rn(bil(pp, P.pitch, P.w, P.h, sx[k], __fadd_rn(sy[k], 1.0f)),
+                                            bil(pp, P.pitch, P.w, P.h, sx[k], __fsub_rn(sy[k], 1.0f))), 0.5f);
+                gxx = __fadd_rn(gxx, __fmul_rn(Ix[k], Ix[k]));
+                gxy = __fadd_rn(gxy, __fmul_rn(Ix[k], Iy[k]));
+                gyy = __fadd_rn(gyy, __fmul_rn(Iy[k], Iy[k]));
+            }
+        }
+        gxx = warp_sum(gxx);
+        gxy = warp_sum(gxy);
+        gyy = warp_sum(gyy);
+        const float dd = __fsub_rn(gxx, gyy);
+        const float lam = __fmul_rn(__fsub_rn(__fadd_rn(gxx, gyy),
+                                              __fsqrt_rn(__fadd_rn(__fmul_rn(dd, dd), __fmul_rn(4.0f, __fmul_rn(gxy, gxy))))),
+                                    0.5f);
+        const float det = __fsub_rn(__fmul_rn(gxx, gyy), __fmul_rn(gxy, gxy));
+        float vx = 0.0f, vy = 0.0f;
+        if (__fdiv_rn(lam, (float)nsamp) < a.min_eig || !(det > 0.0f)) {
+            if (L == 0) { ok = false; break; }
+            gx = __fmul_rn(2.0f, gx);                    // a coarse level without texture: skipped
+            gy = __fmul_rn(2.0f, gy);
+            continue;
+        }
+        for (int it = 0; it < a.max_iters; ++it) {
+            float bx = 0.0f, by = 0.0f;
+            const float ox = __fadd_rn(gx, vx), oy = __fadd_rn(gy, vy);
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                if (lane + 32 * k < nsamp) {
+                    const float e = __fsub_rn(I[k], bil(qp, Q.pitch, Q.w, Q.h, __fadd_rn(sx[k], ox), __fadd_rn(sy[k], oy)));
+                    bx = __fadd_rn(bx, __fmul_rn(e, Ix[k]));
+                    by = __fadd_rn(by, __fmul_rn(e, Iy[k]));
+                }
+            }
+            bx = warp_sum(bx);
+            by = warp_sum(by);
+            const float dx = __fdiv_rn(__fsub_rn(__fmul_rn(gyy, bx), __fmul_rn(gxy, by)), det);
+            const float dy = __fdiv_rn(__fsub_rn(__fmul_rn(gxx, by), __fmul_rn(gxy, bx)), det);
+            vx = __fadd_rn(vx, dx);
+            vy = __fadd_rn(vy, dy);
+            if (L == 0) {
+                const float qx = __fadd_rn(plx, __fadd_rn(gx, vx)), qy = __fadd_rn(ply, __fadd_rn(gy, vy));
+                if (!(qx >= 0.0f && qx < (float)P.w && qy >= 0.0f && qy < (float)P.h)) { ok = false; break; }
+            }
+            if (__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)) < a.eps2) break;
+        }
+        if (!ok) break;
+        if (L > 0) {
+            gx = __fmul_rn(2.0f, __fadd_rn(gx, vx));
+            gy = __fmul_rn(2.0f, __fadd_rn(gy, vy));
+        } else {
+            gx = __fadd_rn(gx, vx);
+            gy = __fadd_rn(gy, vy);
+        }
+    }
+    if (lane == 0) {
+        a.status[o] = ok ? 1 : 0;
+        a.tracked[2 * o] = ok ? __fadd_rn(cx, gx) : __int_as_float(0x7fc00000);
+        a.tracked[2 * o + 1] = ok ? __fadd_rn(cy, gy) : __int_as_float(0x7fc00000);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K5: tracked pairs -> matches (src = frame-t point, dst = frame-(t-1) corner centre)
+// ---------------------------------------------------------------------------------------
+struct CompactArgs {
+    const int* corners;
+    const int* counts;
+    const float* tracked;
+    const uint8_t* status;
+    int max_corners, S;
+    double* src;    // [S][max_corners][2]
+    double* dst;
+    int* mcount;    // [S]
+};
+
+__global__ void klt_compact_kernel(const CompactArgs a) {
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (s >= a.S) return;
+    const int cnt = a.counts[s];
+    int n = 0;
+    for (int b = 0; b < cnt; b += 32) {
+        const int i = b + lane;
+        const long long o = (long long)s * a.max_corners + i;
+        const bool st = i < cnt && a.status[o];
+        const unsigned bal = __ballot_sync(0xffffffffu, st);
+        if (st) {
+            const long long w = (long long)s * a.max_corners + n + __popc(bal & ((1u << lane) - 1u));
+            a.src[2 * w] = (double)a.tracked[2 * o];
+            a.src[2 * w + 1] = (double)a.tracked[2 * o + 1];
+            a.dst[2 * w] = (double)a.corners[2 * o] + 0.5;
+            a.dst[2 * w + 1] = (double)a.corners[2 * o + 1] + 0.5;
+        }
+        n += __popc(bal);
+    }
+    if (lane == 0) a.mcount[s] = n;
+}
+
+// ---------------------------------------------------------------------------------------
+// K6: RANSAC hypotheses (R42), one warp per (stream, iteration)
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ bool ransac_sample(unsigned long long seed, int it, int n, int (&idx)[4]) {
+    int got = 0;
+    for (int k = 0; k < 64 && got < 4; ++k) {
+        const unsigned long long z = splitmix64((seed << 32) + (unsigned long long)it * 64ull + (unsigned long long)k);
+        const int i = (int)(((z >> 32) * (unsigned long long)n) >> 32);
+        bool dup = false;
+        for (int j = 0; j < got; ++j) dup |= idx[j] == i;
+        if (!dup) idx[got++] = i;
+    }
+    return got == 4;
+}
+
+__device__ __forceinline__ bool collinear4(const double (&px)[4], const double (&py)[4]) {
+    double xmin = px[0], xmax = px[0], ymin = py[0], ymax = py[0];
+    for (int k = 1; k < 4; ++k) {
+        xmin = fmin(xmin, px[k]); xmax = fmax(xmax, px[k]);
+        ymin = fmin(ymin, py[k]); ymax = fmax(ymax, py[k]);
+    }
+    const double ext = fmax(fmax(__dsub_rn(xmax, xmin), __dsub_rn(ymax, ymin)), 1e-12);
+    const double lim = __dmul_rn(__dmul_rn(1e-6, ext), ext);
+    for (int p = 0; p < 4; ++p)
+        for (int q = p + 1; q < 4; ++q)
+            for (int r = q + 1; r < 4; ++r) {
+                const double ux = __dsub_rn(px[q], px[p]), uy = __dsub_rn(py[q], py[p]);
+                const double vx = __dsub_rn(px[r], px[p]), vy = __dsub_rn(py[r], py[p]);
+                if (fabs(__dsub_rn(__dmul_rn(ux, vy), __dmul_rn(uy, vx))) <= lim) return true;
+            }
+    return false;
+}
+
+// The homography (h8 = 1) through 4 correspondences: 8x8 system, Gaussian elimination with
+// partial pivoting in fp64.  false for a degenerate sample.
+__device__ bool minimal_h(const double (&x)[4], const double (&y)[4], const double (&u)[4], const double (&v)[4],
+                          double (&h)[9]) {
+    if (collinear4(x, y) || collinear4(u, v)) return false;
+    double A[8][9];
+    for (int i = 0; i < 4; ++i) {
+        double* r0 = A[2 * i];
+        double* r1 = A[2 * i + 1];
+        r0[0] = x[i]; r0[1] = y[i]; r0[2] = 1.0; r0[3] = 0.0; r0[4] = 0.0; r0[5] = 0.0;
+        r0[6] = -__dmul_rn(u[i], x[i]); r0[7] = -__dmul_rn(u[i], y[i]); r0[8] = u[i];
+        r1[0] = 0.0; r1[1] = 0.0; r1[2] = 0.0; r1[3] = x[i]; r1[4] = y[i]; r1[5] = 1.0;
+        r1[6] = -__dmul_rn(v[i], x[i]); r1[7] = -__dmul_rn(v[i], y[i]); r1[8] = v[i];
+    }
+    for (int c = 0; c < 8; ++c) {
+        int piv = c;
+        double best = fabs(A[c][c]);
+        for (int r = c + 1; r < 8; ++r)
+            if (fabs(A[r][c]) > best) { best = fabs(A[r][c]); piv = r; }
+        if (!(best > 0.0)) return false;
+        if (piv != c)
+            for (int k = 0; k < 9; ++k) { const double t = A[c][k]; A[c][k] = A[piv][k]; A[piv][k] = t; }
+        for (int r = c + 1; r < 8; ++r) {
+            const double f = __ddiv_rn(A[r][c], A[c][c]);
+            for (int k = c + 1; k < 9; ++k) A[r][k] = __dsub_rn(A[r][k], __dmul_rn(f, A[c][k]));
+        }
+    }
+    for (int r = 7; r >= 0; --r) {
+        double acc = A[r][8];
+        for (int k = r + 1; k < 8; ++k) acc = __dsub_rn(acc, __dmul_rn(A[r][k], h[k]));
+        h[r] = __ddiv_rn(acc, A[r][r]);
+    }
+    h[8] = 1.0;
+    return true;
+}
+
+__device__ __forceinline__ double reproj_err2(const double (&h)[9], double x, double y, double u, double v) {
+    const double w = __dadd_rn(__dadd_rn(__dmul_rn(h[6], x), __dmul_rn(h[7], y)), h[8]);
+    const double px = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(h[0], x), __dmul_rn(h[1], y)), h[2]), w);
+    const double py = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(h[3], x), __dmul_rn(h[4], y)), h[5]), w);
+    const double ex = __dsub_rn(px, u), ey = __dsub_rn(py, v);
+    return __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+}
+
+struct RansacArgs {
+    const double* src;    // [S][max_corners][2]
+    const double* dst;
+    const int* mcount;    // [S]
+    int max_corners, iters;
+    unsigned long long seed;
+    double thresh2;
+    int* iter_counts;     // [S][iters]
+};
+
+__global__ void __launch_bounds__(128) klt_ransac_kernel(const RansacArgs a) {
+    const int it = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31, s = blockIdx.y;
+    if (it >= a.iters) return;
+    const int n = a.mcount[s];
+    const double* src = a.src + (long long)s * a.max_corners * 2;
+    const double* dst = a.dst + (long long)s * a.max_corners * 2;
+    int result = -1;
+    int idx[4];
+    double h[9];
+    if (n >= 4 && ransac_sample(a.seed, it, n, idx)) {
+        double x[4], y[4], u[4], v[4];
+        for (int k = 0; k < 4; ++k) {
+            x[k] = src[2 * idx[k]]; y[k] = src[2 * idx[k] + 1];
+            u[k] = dst[2 * idx[k]]; v[k] = dst[2 * idx[k] + 1];
+        }
+        if (minimal_h(x, y, u, v, h)) {
+            int c = 0;
+            for (int j = lane; j < n; j += 32)
+                c += reproj_err2(h, src[2 * j], src[2 * j + 1], dst[2 * j], dst[2 * j + 1]) < a.thresh2;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            result = c;
+        }
+    }
+    if (lane == 0) a.iter_counts[(long long)s * a.iters + it] = result;
+}
+
+// ---------------------------------------------------------------------------------------
+// K7: best model -> inliers -> normalized DLT (R41), one warp per stream
+// ---------------------------------------------------------------------------------------
+struct RefitArgs {
+    const double* src;
+    const double* dst;
+    const int* mcount;
+    const int* iter_counts;
+    int max_corners, iters, S;
+    unsigned long long seed;
+    double thresh2;
+    double* H_out;          // [S][9]
+    uint8_t* inliers;       // [S][max_corners] (may be null)
+    int* ok_out;            // [S] (may be null)
+};
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Smallest-eigenvalue eigenvector of a symmetric 9x9 matrix by cyclic Jacobi in fp64, one
+// warp: every rotation (p, q) updates columns p, q (lane k: row k), then rows p, q (lane k:
+// column k) and the eigenvectors -- lanes 0..8 in parallel on the warp's shared-memory copy.
+// Sweeps stop when the off-diagonal mass is below 1e-30 of the total (roundoff level).
+__device__ void min_eigvec9_warp(double* m, double* V, int lane, double* out) {
+    if (lane < 9)
+        for (int j = 0; j < 9; ++j) V[lane * 9 + j] = lane == j ? 1.0 : 0.0;
+    __syncwarp();
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        double off = 0.0, tot = 0.0;
+        if (lane < 9)
+            for (int q = 0; q < 9; ++q) {
+                const double x = m[lane * 9 + q];
+                tot += x * x;
+                if (q != lane) off += x * x;
+            }
+        off = warp_sum_d(off);
+        tot = warp_sum_d(tot);
+        if (!(off > 1e-30 * tot)) break;
+        for (int p = 0; p < 8; ++p)
+            for (int q = p + 1; q < 9; ++q) {
+                const double apq = m[p * 9 + q];
+                if (apq == 0.0) continue;                 // uniform: every lane reads the same value
+                const double theta = (m[q * 9 + q] - m[p * 9 + p]) / (2.0 * apq);
+                const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+                __syncwarp();
+                if (lane < 9) {                           // columns p, q
+                    const double kp = m[lane * 9 + p], kq = m[lane * 9 + q];
+                    m[lane * 9 + p] = c * kp - sn * kq;
+                    m[lane * 9 + q] = sn * kp + c * kq;
+                }
+                __syncwarp();
+                if (lane < 9) {                           // rows p, q
+                    const double pk = m[p * 9 + lane], qk = m[q * 9 + lane];
+                    m[p * 9 + lane] = c * pk - sn * qk;
+                    m[q * 9 + lane] = sn * pk + c * qk;
+                    const double vp = V[lane * 9 + p], vq = V[lane * 9 + q];
+                    V[lane * 9 + p] = c * vp - sn * vq;
+                    V[lane * 9 + q] = sn * vp + c * vq;
+                }
+                __syncwarp();
+            }
+    }
+    int best = 0;
+    for (int i = 1; i < 9; ++i)
+        if (m[i * 9 + i] < m[best * 9 + best]) best = i;
+    if (lane < 9) out[lane] = V[lane * 9 + best];
+    __syncwarp();
+}
+
+__global__ void klt_refit_kernel(const RefitArgs a) {
+    __shared__ double sm_m[4][81], sm_v[4][81], sm_e[4][9];
+    const int w = threadIdx.x >> 5;
+    const int s = blockIdx.x * (blockDim.x >> 5) + w, lane = threadIdx.x & 31;
+    if (s >= a.S) return;
+    const int n = a.mcount[s];
+    const double* src = a.src + (long long)s * a.max_corners * 2;
+    const double* dst = a.dst + (long long)s * a.max_corners * 2;
+    double* Ho = a.H_out + 9 * (long long)s;
+    // best iteration: most inliers, ties to the earliest
+    int best = -1, bit = -1;
+    for (int j = lane; j < a.iters; j += 32) {
+        const int c = a.iter_counts[(long long)s * a.iters + j];
+        if (c > best) { best = c; bit = j; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int ob = __shfl_xor_sync(0xffffffffu, best, o), oi = __shfl_xor_sync(0xffffffffu, bit, o);
+        if (ob > best || (ob == best && oi < bit && oi >= 0)) { best = ob; bit = oi; }
+    }
+    bool okm = best >= 4 && n >= 4;
+    double h[9];
+    if (okm) {
+        int idx[4];
+        double x[4], y[4], u[4], v[4];
+        ransac_sample(a.seed, bit, n, idx);
+        for (int k = 0; k < 4; ++k) {
+            x[k] = src[2 * idx[k]]; y[k] = src[2 * idx[k] + 1];
+            u[k] = dst[2 * idx[k]]; v[k] = dst[2 * idx[k] + 1];
+        }
+        okm = minimal_h(x, y, u, v, h);
+    }
+    if (!okm) {
+        if (lane < 9) Ho[lane] = (lane % 4 == 0) ? 1.0 : 0.0;
+        for (int j = lane; j < n && a.inliers; j += 32) a.inliers[(long long)s * a.max_corners + j] = 0;
+        if (lane == 0 && a.ok_out) a.ok_out[s] = 0;
+        return;
+    }
+    // inliers of the best model; Hartley normalisation of both sets over them
+    double sx = 0, sy = 0, su = 0, sv = 0, cnt = 0;
+    for (int j = lane; j < n; j += 32) {
+        const bool in = reproj_err2(h, src[2 * j], src[2 * j + 1], dst[2 * j], dst[2 * j + 1]) < a.thresh2;
+        if (a.inliers) a.inliers[(long long)s * a.max_corners + j] = in;
+        if (in) { sx += src[2 * j]; sy += src[2 * j + 1]; su += dst[2 * j]; sv += dst[2 * j + 1]; cnt += 1.0; }
+    }
+    cnt = warp_sum_d(cnt);
+    const double mx = warp_sum_d(sx) / cnt, my = warp_sum_d(sy) / cnt;
+    const double mu = warp_sum_d(su) / cnt, mv = warp_sum_d(sv) / cnt;
+    double ds = 0, dd = 0;
+    for (int j = lane; j < n; j += 32) {
+        if (reproj_err2(h, src[2 * j], src[2 * j + 1], dst[2 * j], dst[2 * j + 1]) < a.thresh2) {
+            ds += sqrt((src[2 * j] - mx) * (src[2 * j] - mx) + (src[2 * j + 1] - my) * (src[2 * j + 1] - my));
+            dd += sqrt((dst[2 * j] - mu) * (dst[2 * j] - mu) + (dst[2 * j + 1] - mv) * (dst[2 * j + 1] - mv));
+        }
+    }
+    ds = warp_sum_d(ds) / cnt;
+    dd = warp_sum_d(dd) / cnt;
+    const double ks = ds > 0 ? sqrt(2.0) / ds : 1.0, kd = dd > 0 ? sqrt(2.0) / dd : 1.0;
+    // A^T A of the normalized system, 45 distinct entries per lane, then the warp sum
+    double M[45];
+#pragma unroll
+    for (int k = 0; k < 45; ++k) M[k] = 0.0;
+    for (int j = lane; j < n; j += 32) {
+        if (!(reproj_err2(h, src[2 * j], src[2 * j + 1], dst[2 * j], dst[2 * j + 1]) < a.thresh2)) continue;
+        const double X = ks * (src[2 * j] - mx), Y = ks * (src[2 * j + 1] - my);
+        const double U = kd * (dst[2 * j] - mu), Vv = kd * (dst[2 * j + 1] - mv);
+        const double r1[9] = {0, 0, 0, -X, -Y, -1, Vv * X, Vv * Y, Vv};
+        const double r2[9] = {X, Y, 1, 0, 0, 0, -U * X, -U * Y, -U};
+        int k = 0;
+#pragma unroll
+        for (int p = 0; p < 9; ++p)
+#pragma unroll
+            for (int q = p; q < 9; ++q) M[k++] += r1[p] * r1[q] + r2[p] * r2[q];
+    }
+#pragma unroll
+    for (int k = 0; k < 45; ++k) M[k] = warp_sum_d(M[k]);
+    double* m = sm_m[w];
+    if (lane == 0) {
+        int k = 0;
+        for (int p = 0; p < 9; ++p)
+            for (int q = p; q < 9; ++q) { m[p * 9 + q] = M[k]; m[q * 9 + p] = M[k]; ++k; }
+    }
+    __syncwarp();
+    min_eigvec9_warp(m, sm_v[w], lane, sm_e[w]);
+    if (lane == 0) {
+        const double* e = sm_e[w];
+        // H = Td^-1 Hn Ts, Ts = [[ks,0,-ks mx],[0,ks,-ks my],[0,0,1]], Td^-1 = [[1/kd,0,mu],[0,1/kd,mv],[0,0,1]]
+        double T[9];   // Hn Ts
+        for (int r = 0; r < 3; ++r) {
+            T[3 * r + 0] = e[3 * r + 0] * ks;
+            T[3 * r + 1] = e[3 * r + 1] * ks;
+            T[3 * r + 2] = -e[3 * r + 0] * ks * mx - e[3 * r + 1] * ks * my + e[3 * r + 2];
+        }
+        double R[9];
+        for (int c = 0; c < 3; ++c) {
+            R[0 + c] = T[0 + c] / kd + mu * T[6 + c];
+            R[3 + c] = T[3 + c] / kd + mv * T[6 + c];
+            R[6 + c] = T[6 + c];
+        }
+        const double z = R[8];
+        for (int q = 0; q < 9; ++q) Ho[q] = R[q] / z;
+        if (a.ok_out) a.ok_out[s] = (int)cnt;
+    }
+}
+
+}  // namespace dmsgm_klt

@@ -19,20 +19,31 @@ def built():
     return build.build()
 
 
-def _declared():
-    src = open(os.path.join(ROOT, "include", "dmsgm.h")).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(dmsgm_[a-z_]+)\s*\(", src)))
+HEADERS = ("dmsgm.h", "dmsgm_klt.h")
+
+
+def _declared(header=None):
+    names = set()
+    for h in ([header] if header else HEADERS):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(dmsgm_[a-z_]+)\s*\(", src))
+    return sorted(names)
+
+
+def test_every_header_is_checked():
+    assert sorted(f for f in os.listdir(os.path.join(ROOT, "include")) if f.endswith(".h")) == sorted(HEADERS)
 
 
 def test_header_exports(built):
     lib = ctypes.CDLL(built)
     names = _declared()
-    assert len(names) >= 12, names
+    assert len(names) >= 22, names
     for n in names:
-        assert hasattr(lib, n), f"{n} declared in include/dmsgm.h but not exported"
+        assert hasattr(lib, n), f"{n} declared in include/ but not exported"
     import paper_1702_05156_b200 as dm
-    assert sorted(dm.EXPORTS) == names
+    assert sorted(dm.EXPORTS) == _declared("dmsgm.h")
+    assert sorted(dm.KLT_EXPORTS) == _declared("dmsgm_klt.h")
 
 
 def test_symbols_are_c_linkage(built):
@@ -58,6 +69,16 @@ def test_version_and_argument_errors(built):
     assert lib.dmsgm_create(64, 48, 4, ctypes.byref(big), 0, ctypes.byref(h)) == dm.DMSGM_EINVAL
     assert b"age_cap" in lib.dmsgm_last_error(None)
     assert lib.dmsgm_step(None, None, 64, None, None, 64, None) == dm.DMSGM_EINVAL
+    # include/dmsgm_klt.h: parameter errors before any CUDA call
+    from paper_1702_05156_b200 import klt
+    L = klt._setup(lib)
+    for bad in (dm.KltParams(win=2), dm.KltParams(max_corners=5000), dm.KltParams(quality=0.0),
+                dm.KltParams(max_level=6), dm.KltParams(min_distance=0.5), dm.KltParams(ransac_iters=0)):
+        cp = bad.to_c()
+        assert L.dmsgm_klt_create(640, 480, ctypes.byref(cp), 0, ctypes.byref(h)) == dm.DMSGM_EINVAL
+    cp = dm.KltParams().to_c()
+    assert L.dmsgm_klt_create(4, 480, ctypes.byref(cp), 0, ctypes.byref(h)) == dm.DMSGM_EINVAL
+    assert L.dmsgm_klt_estimate(None, None, 64, None, 64, None, None, None) == dm.DMSGM_EINVAL
 
 
 def test_no_gpu_fails_cleanly(built):
