@@ -162,7 +162,7 @@ void dmsgm_destroy(dmsgm_ctx* ctx);
 /* ------------------------------------------------------------------------------------
  * Frame preprocessing: PAPER.md §2.1 pre-processes
  * the incoming frame with "a Gaussian filter and a median filter"; §3.3.1
- * and App. A/B give the implementation.  DESIGN.md readings R30-R34: separable Gaussian
+ * and App. C/D give the implementation.  DESIGN.md readings R30-R34: separable Gaussian
  * of odd size gauss_size (1 = off, 3, 5, 7) and std gauss_sigma > 0 in fp32 (row pass,
  * then column pass rounded once to u8), then the clamped 3x3 median (median_radius 1;
  * 0 = off); image borders clamp.

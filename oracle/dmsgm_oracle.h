@@ -84,7 +84,7 @@ int dmsgm_oracle_set_tilde_probe(dmsgm_oracle_ctx* ctx, float* buf);
 /* The decay factor exp(-lambda * d) of reading R18 (form 0; exposed for its pin). */
 float dmsgm_oracle_decay_factor(float lambda, float d);
 
-/* Frame preprocessing of §2.1 / §3.3.1 / App. A-B (prefilter_oracle.c, readings R30-R34):
+/* Frame preprocessing of §2.1 / §3.3.1 / App. C-D (prefilter_oracle.c, readings R30-R34):
  * the normalised Gaussian taps (size odd <= 15, sigma > 0), and the separable Gaussian
  * (gauss_size 1 = off) followed by the clamped median of radius median_radius
  * (0 = off, <= 4) of one u8 frame. */

@@ -2,24 +2,24 @@
  * prefilter_oracle.c -- TEST INFRASTRUCTURE ONLY (part of the oracle library).
  *
  * The frame preprocessing of PAPER.md §2.1 as the paper implements it on the
- * GPU (§3.3.1, App. B P:545-567 Gaussian, App. A P:569-589 median), written
+ * GPU (§3.3.1, App. C P:545-567 Gaussian, App. D P:569-589 median), written
  * out step by step; the readings R30-R34 of DESIGN.md §2 fix what the paper leaves open:
  *
  *   R30 taps: w_i = exp(-(i-c)^2 / (2 sigma^2)), c = (k-1)/2, i = 0..k-1 (Eq. 1; its
  *       1/(sigma sqrt(2 pi)) factor cancels in the normalisation), computed and
  *       normalised to sum 1 in double, then rounded to float.
  *   R31 separable (§3.3.1 "convolve first the rows and then the columns"): each pass
- *       is App. B's loop over the 1-D window, blur = 0.f; blur += pixel * weight in
+ *       is App. C's loop over the 1-D window, blur = 0.f; blur += pixel * weight in
  *       ascending tap order, evaluated as fmaf(pixel, weight, blur) (the contraction
  *       nvcc applies to the paper's CUDA code).  The row pass's result stays float
  *       (real arithmetic between the passes); the column pass's sum is rounded to the
  *       nearest integer (ties to even) and clamped to [0, 255] -- ONE quantization to the
- *       u8 frame the model consumes.  (App. B's static_cast<unsigned char> truncation,
+ *       u8 frame the model consumes.  (App. C's static_cast<unsigned char> truncation,
  *       applied after each pass, would darken a constant frame by up to 2 grey levels
  *       whenever the float taps sum below 1; DESIGN.md records the choice.)
- *   R32 borders: App. A/B "Clamp filter to the image border", to the last valid index.
+ *   R32 borders: App. C/D "Clamp filter to the image border", to the last valid index.
  *   R33 median: the 3x3 window ("the surrounding 8 pixels ... as well as the current
- *       pixel", §3.1.1), clamped, its middle order statistic (App. A sorts the
+ *       pixel", §3.1.1), clamped, its middle order statistic (App. D sorts the
  *       window and takes window[len/2]).
  *   R34 order: Gaussian, then median, on the raw frame; the result replaces the frame
  *       for the whole DMSGM step (S4 and S8).
@@ -77,7 +77,7 @@ static void gauss_cols(int width, int height, const float* in, uint8_t* out, siz
         }
 }
 
-/* R33: insertion sort of the clamped (2 radius + 1)^2 window, middle element (App. A). */
+/* R33: insertion sort of the clamped (2 radius + 1)^2 window, middle element (App. D). */
 static void median_filter(int width, int height, const uint8_t* in, size_t in_pitch, uint8_t* out,
                           size_t out_pitch, int radius) {
     uint8_t window[81];

@@ -1,5 +1,5 @@
 // dmsgm_prefilter.cuh -- the optional frame preprocessing of the step:
-// separable Gaussian then 3x3 median (§2.1, §3.3.1, App. A/B;
+// separable Gaussian then 3x3 median (§2.1, §3.3.1, App. C/D;
 // readings R30-R34 of DESIGN.md §2).
 //
 // One streaming kernel (see dmsgm_prefilter_kernel below): a warp walks a 120-column strip
