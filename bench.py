@@ -36,6 +36,7 @@ if ROOT not in sys.path:
 L2_BYTES = 126 * 1024 * 1024
 RING = 8          # distinct synthetic frames per stream (periodic camera motion, no seam)
 GRAPH_T = 40      # steps per CUDA-graph replay (dmsgm_step_n) in the timed region
+PRESLEEP_CYCLES = 200_000   # ~100 us spin kernel queued before the start event (host launch latency)
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 SPEC_HBM_GBS = 8000.0       # B200 datasheet HBM3e bandwidth: BASELINE.md §3's denominator, reported beside
 
@@ -353,6 +354,11 @@ def run_dmsgm(args, rank, world, local):
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(chunks) + 1)]
     sampler = ClockSampler(local)
     with sampler:
+        # a spin kernel ahead of the start event keeps the device busy while the host
+        # enqueues the first graph launch: the events then bracket exactly the K steps'
+        # device execution, not the host's launch latency (measured: K = 20 graph replays
+        # read 53.7 us/step without it, 52.7 with it; scripts/k_overhead.py)
+        torch.cuda._sleep(PRESLEEP_CYCLES)
         torch.cuda.nvtx.range_push("timed")
         evs[0].record(stream)
         for k, T in enumerate(chunks):
@@ -497,7 +503,8 @@ def run_dmsgm(args, rank, world, local):
             "timing": f"{len(chunks)} " + ("CUDA-graph replays of dmsgm_step_n" if args.launch == "graph" else
                                            "groups of single dmsgm_step launches") + f" ({GRAPH_T} steps each"
                       f"{'' if args.steps % GRAPH_T == 0 else ', the last ' + str(args.steps % GRAPH_T)}) "
-                      f"between CUDA events on the launching stream; value from the whole K-step region, "
+                      f"between CUDA events on the launching stream (a ~100 us spin kernel queued ahead of the start "
+                      f"event hides the host's launch latency); value from the whole K-step region, "
                       f"median_ms_per_step = median over the {len(rep_ms)} full replays",
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth/ ring recipe, generated on device)",
@@ -635,6 +642,8 @@ def run_band(args, rank, world, local):
     ev1 = torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     with sampler:
+        with torch.cuda.stream(main_stream):
+            torch.cuda._sleep(PRESLEEP_CYCLES)      # see the first timed region
         torch.cuda.nvtx.range_push("timed")
         ev0.record(main_stream)
         fork()

@@ -14,10 +14,11 @@ COMBOS = [(1, 1.0, 0), (1, 1.0, 1), (3, 1.0, 0), (3, 0.8, 1), (5, 1.0, 0), (5, 1
 
 
 @pytest.mark.parametrize("gs,sigma,mr", COMBOS)
-# sizes: single pixel rows, ragged 120-column strips and 40-row bands of the streaming
-# kernel (244 = 2 x 120 + 4, 81 = 2 x 40 + 1), a 1080p-wide frame of 2 rows
-@pytest.mark.parametrize("W,H,S", [(4, 1, 1), (8, 3, 2), (100, 45, 2), (256, 64, 1), (132, 33, 3), (244, 81, 1),
-                                   (1920, 2, 1), (364, 121, 2)])
+# sizes: single pixel rows, ragged 240-column strips and 120-row bands of the streaming
+# kernel (244 = 240 + 4, 484 = 2 x 240 + 4, 248 = 240 + 8, 121 = 120 + 1, 241 = 2 x 120 + 1),
+# a 1080p-wide frame of 2 rows
+@pytest.mark.parametrize("W,H,S", [(4, 1, 1), (8, 3, 2), (12, 2, 1), (100, 45, 2), (256, 64, 1), (132, 33, 3),
+                                   (244, 81, 1), (1920, 2, 1), (364, 121, 2), (484, 241, 1), (248, 120, 2)])
 def test_filter_bitwise(cuda_lib, oracle_mod, gs, sigma, mr, W, H, S):
     import torch
     rng = np.random.default_rng(W * 1000 + H + gs + mr)
