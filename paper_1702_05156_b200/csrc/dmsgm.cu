@@ -324,7 +324,21 @@ cudaError_t launch_warp(int W, int H, int count, const uint8_t* in, long long in
     const long long resident = (long long)kWarpCtasPerSm * sms;   // every CTA resident: contiguous tile ranges
     const int grid = (int)(tiles < resident ? tiles : resident);
     if (grid == 0) return cudaSuccess;
-    dmsgm_warp_kernel<<<grid, kWarpThreads, kWarpDynSmem, stream>>>(a);
+    // the frame batch as u16 {W/2, H, streams} for the TMA box copies (16-byte aligned rows
+    // and streams required; otherwise the kernel copies every box row by row)
+    CUtensorMap map = {};
+    a.tma = 0;
+    auto enc = tensor_map_encoder();
+    if (enc && (in_pitch & 15) == 0 && ((uintptr_t)in & 15) == 0 && (in_stride & 15) == 0) {
+        cuuint64_t dims[3] = {(cuuint64_t)W / 2, (cuuint64_t)H, (cuuint64_t)count};
+        cuuint64_t strides[2] = {(cuuint64_t)in_pitch, (cuuint64_t)in_stride};
+        cuuint32_t box[3] = {(cuuint32_t)kWarpBoxPitch / 2, (cuuint32_t)kWarpTmaRows, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        a.tma = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, (void*)in, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    dmsgm_warp_kernel<<<grid, kWarpThreads, kWarpDynSmem, stream>>>(a, map);
     return cudaGetLastError();
 }
 
