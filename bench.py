@@ -87,6 +87,39 @@ def ncu_instructions(name, pixels=None):
     return c4 * pixels / (32 * 1920 * 1080) if c4 else None
 
 
+# Minimal thread-instructions per pixel of the filter and warp kernels (DESIGN.md §6.4 / §6.5):
+# the operations their readings fix, counted as one instruction per paired fp32 operation
+# (two pixels per FFMA2 / FADD2), one per byte conversion, load or 16-bit-lane min/max.
+def prefilter_min_instr_per_px(g, m):
+    gauss = (2 * g + 1) + 1.5 + 1.0 if g > 0 else 0.0   # R31: 2(2g+1) fma / 2 + u8->f32 + rint->u8
+    median = 7.0 if m else 0.0                           # R33: sorted columns 2 + merge 5 (16-bit lanes)
+    return gauss + median
+
+
+WARP_MIN_INSTR_PER_PX = 23.0   # R36/R37: 26 fp32 ops paired (13) + 4 tap loads + 4 conversions + pack/address 2
+
+
+def work_roofline(kernel, ms, pixels, min_per_px, instr, sms, mhz, peak_hbm, hbm_bytes, traffic, share, src):
+    """A filter / warp kernel against HBM (its algorithmic 2 B/px) and against the issue
+    time of its minimal instruction count: `roofline` carries the HBM
+    view, `work` the instruction view (achieved = minimal instructions / time)."""
+    peak_issue = sms * 4 * mhz * 1e6 / 1e9            # warp-instructions / ns (4 schedulers per SM)
+    min_instr = min_per_px * pixels / 32.0             # warp-instructions per launch
+    hbm = hbm_bytes / (ms * 1e-3) / 1e9
+    return {
+        "bound": "hbm", "achieved": hbm, "peak": peak_hbm, "unit": "GB/s", "frac": hbm / peak_hbm,
+        "traffic": traffic, "algorithmic_bytes_per_launch": hbm_bytes, "kernel": kernel, "ms_per_launch": ms,
+        "share_of_step": share,
+        "work": {"bound": "alu", "unit": "G warp-inst/s", "peak": peak_issue,
+                 "min_instr_per_px": min_per_px, "min_instructions_per_launch": min_instr,
+                 "achieved": min_instr / (ms * 1e-3) / 1e9, "frac": min_instr / (ms * 1e-3) / 1e9 / peak_issue,
+                 "measured_instructions_per_launch": instr,
+                 "instr_efficiency": (min_instr / instr) if instr else None,
+                 "peak_source": f"{sms} SMs x 4 schedulers x 1 warp-instruction/clock x {mhz:.0f} MHz",
+                 "instr_source": src},
+    }
+
+
 def ncu_traffic(workload):
     """dram bytes per launch from the committed ncu --set full capture (profiles/), or None."""
     path = os.path.join(ROOT, "profiles", f"ncu_traffic_{workload}.json")
@@ -452,15 +485,11 @@ def run_dmsgm(args, rank, world, local):
         pf_ms = p0.elapsed_time(p1) / kpf
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965
-        peak_issue = sms * 4 * mhz * 1e6 / 1e9          # warp-instructions / ns (4 schedulers per SM)
         instr = ncu_instructions(f"prefilter_{args.config}", pixels=S * W * H)
-        pf_roof = {"bound": "alu", "unit": "G warp-inst/s", "peak": peak_issue,
-                   "achieved": instr / (pf_ms * 1e-3) / 1e9 if instr else None,
-                   "frac": instr / (pf_ms * 1e-3) / 1e9 / peak_issue if instr else None,
-                   "traffic": None, "kernel": "dmsgm_prefilter_kernel", "ms_per_launch": pf_ms,
-                   "share_of_step": pf_ms / ms_per_step, "instructions_per_launch": instr,
-                   "peak_source": f"{sms} SMs x 4 schedulers x 1 warp-instruction/clock x {mhz:.0f} MHz "
-                                  "(DESIGN.md §6.4)"}
+        pf_roof = work_roofline("dmsgm_prefilter_kernel", pf_ms, S * W * H, prefilter_min_instr_per_px(
+            (pf[0] - 1) // 2, pf[2]), instr, sms, mhz, peak, 2.0 * S * W * H, None, pf_ms / ms_per_step,
+            "profiles/ncu_instr_prefilter_C4.json (scaled by pixels for other workloads)")
+        pf_roof["peak_source"] = peak_src
     warp_roof = None
     if args.motion == "frame":
         # the frame-warp kernel alone (CUDA events on the launching stream)
@@ -475,22 +504,13 @@ def run_dmsgm(args, rank, world, local):
         p1.record(stream)
         p1.synchronize()
         w_ms = p0.elapsed_time(p1) / kw
-        wbytes = 2.0 * S * W * H
-        # ALU-bound: reported against the issue rate like the prefilter;
-        # the HBM figure (2 B/px) is kept beside it
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965
-        peak_issue = sms * 4 * mhz * 1e6 / 1e9          # warp-instructions / ns (4 schedulers per SM)
         instr = ncu_instructions(f"warp_{args.config}", pixels=S * W * H)
-        warp_roof = {"bound": "alu", "unit": "G warp-inst/s", "peak": peak_issue,
-                     "achieved": instr / (w_ms * 1e-3) / 1e9 if instr else None,
-                     "frac": instr / (w_ms * 1e-3) / 1e9 / peak_issue if instr else None,
-                     "traffic": None, "kernel": "dmsgm_warp_kernel", "ms_per_launch": w_ms,
-                     "share_of_step": w_ms / ms_per_step, "instructions_per_launch": instr,
-                     "hbm_gbs": wbytes / (w_ms * 1e-3) / 1e9, "hbm_frac": wbytes / (w_ms * 1e-3) / 1e9 / peak,
-                     "algorithmic_bytes_per_launch": wbytes,
-                     "peak_source": f"{sms} SMs x 4 schedulers x 1 warp-instruction/clock x {mhz:.0f} MHz "
-                                    "(DESIGN.md §6.5)"}
+        warp_roof = work_roofline("dmsgm_warp_kernel", w_ms, S * W * H, WARP_MIN_INSTR_PER_PX, instr, sms, mhz, peak,
+                                  2.0 * S * W * H, None, w_ms / ms_per_step,
+                                  "profiles/ncu_instr_warp_C4.json (scaled by pixels for other workloads)")
+        warp_roof["peak_source"] = peak_src
     kernel_name = info.kernel.decode()
     ctx.close()
     if rank == 0:

@@ -40,3 +40,23 @@ def test_roofline_helpers_read_committed_evidence():
     # a workload without its own capture: the C4 count scaled by the pixel count
     assert abs(bench.ncu_instructions("warp_C4p", pixels=4 * 1920 * 1080) - c4 * 4 / 32) < 1.0
     assert bench.ncu_instructions("warp_C4p") is None
+
+
+def test_work_roofline_reports_hbm_and_minimal_instructions():
+    """The filter / warp kernels are reported against HBM (2 B/px) and against the issue
+    time of their minimal instruction count, not against executed
+    instructions: a faster kernel raises both fractions, a kernel executing more
+    instructions for the same time raises neither."""
+    import bench
+    assert bench.prefilter_min_instr_per_px(2, 1) == 5 + 1.5 + 1 + 7
+    assert bench.prefilter_min_instr_per_px(0, 1) == 7
+    assert bench.prefilter_min_instr_per_px(1, 0) == 3 + 2.5
+    px = 32 * 1920 * 1080
+    r = bench.work_roofline("k", 0.080, px, 14.5, 2 * 14.5 * px / 32, 148, 1965.0, 6454.3, 2.0 * px, None, 0.6, "x")
+    assert r["bound"] == "hbm" and abs(r["achieved"] - 2.0 * px / 80e-6 / 1e9) < 1e-6
+    assert abs(r["frac"] - r["achieved"] / 6454.3) < 1e-12
+    w = r["work"]
+    assert abs(w["instr_efficiency"] - 0.5) < 1e-12
+    assert abs(w["achieved"] - 14.5 * px / 32 / 80e-6 / 1e9) < 1e-6
+    r2 = bench.work_roofline("k", 0.080, px, 14.5, 4 * 14.5 * px / 32, 148, 1965.0, 6454.3, 2.0 * px, None, 0.6, "x")
+    assert r2["work"]["frac"] == w["frac"] and r2["frac"] == r["frac"]
