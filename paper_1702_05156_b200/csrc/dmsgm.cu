@@ -189,6 +189,10 @@ cudaError_t setup_staged(dmsgm_ctx* c) {
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     if (e != cudaSuccess) return e;
+    // DMSGM_STAGED_CTAS_PER_SM caps the resident CTAs per SM the persistent grid uses (leaves
+    // room for a concurrent kernel on another stream; scripts/pf_overlap.py)
+    const char* cap = getenv("DMSGM_STAGED_CTAS_PER_SM");
+    if (cap && atoi(cap) > 0 && atoi(cap) < per_sm) per_sm = atoi(cap);
     c->staged_ctas = (per_sm > 0 ? per_sm : 1) * sms;
     for (int i = 0; i < 2; ++i)
         if (!encode_state_map(c, c->state[i], Staged<N, BPT>::XC, Staged<N, BPT>::WROWS, &c->state_map[i]))
@@ -349,6 +353,7 @@ cudaError_t launch_prefilter(int W, int H, int count, const uint8_t* in, long lo
     a.in = in; a.in_stride = in_stride; a.in_pitch = (int)in_pitch;
     a.out = out; a.out_stride = out_stride; a.out_pitch = (int)out_pitch;
     a.W = W; a.H = H; a.g = g; a.m = m;
+    a.one = 1;
     for (int i = 0; i < 2 * kPfMaxG + 1; ++i) a.taps[i] = i < 2 * g + 1 ? taps[i] : 0.0f;
     const int strips = (W + kPfOutW - 1) / kPfOutW;
     const dim3 grid((strips + kPfWarps - 1) / kPfWarps, (H + kPfBand - 1) / kPfBand, count);

@@ -30,6 +30,7 @@ struct PrefilterArgs {
     int g;                        // Gaussian radius (0 = off)
     int m;                        // median radius (0 or 1)
     float taps[2 * kPfMaxG + 1];
+    uint32_t one;                 // 1 (a runtime operand: see pf_sort3)
 };
 
 // Exact fp32 value 2^23 + byte k of w ("magic" float: its low byte is the byte, bytes 1-2
@@ -46,11 +47,29 @@ struct PfSorted {
 };
 // a column triple sorted per lane; the middle one is the sum minus the extremes (lanes <=
 // 3 * 255: no carry or borrow crosses the 16-bit lanes)
-__device__ __forceinline__ PfSorted pf_sort3(uint32_t a, uint32_t b, uint32_t c) {
+#ifndef DMSGM_PF_IMAD_MED
+#define DMSGM_PF_IMAD_MED 0
+#endif
+#ifndef DMSGM_PF_IMAD_SORT
+#define DMSGM_PF_IMAD_SORT 1
+#endif
+__device__ __forceinline__ PfSorted pf_sort3(uint32_t a, uint32_t b, uint32_t c, uint32_t one) {
     PfSorted s;
     s.lo = __vimin3_u16x2(a, b, c);
     s.hi = __vimax3_u16x2(a, b, c);
+#if DMSGM_PF_IMAD_SORT
+    // the sum on the FMA pipe (IMAD x * one + y with `one` = 1 from the kernel parameters,
+    // which ptxas cannot fold into an IADD3): the kernel is bound by the ALU pipe, where the
+    // min / max / PRMT work runs
+    uint32_t t;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(a), "r"(one), "r"(b));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(c), "r"(one), "r"(t));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(s.lo), "r"(0u - one), "r"(t));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s.mi) : "r"(s.hi), "r"(0u - one), "r"(t));
+#else
+    (void)one;
     s.mi = a + b + c - s.lo - s.hi;
+#endif
     return s;
 }
 // Medians of the 3x3 windows of the C output columns x .. x+C-1 (R33).  ra / rb / rc = rows
@@ -61,19 +80,22 @@ __device__ __forceinline__ PfSorted pf_sort3(uint32_t a, uint32_t b, uint32_t c)
 // j+1 and their middle pair (x+2j, x+2j+1) = (hi half of word j, lo half of word j+1).
 template <int C>
 __device__ __forceinline__ void pf_median(const uint32_t (&ra)[C / 2 + 1], const uint32_t (&rb)[C / 2 + 1],
-                                          const uint32_t (&rc)[C / 2 + 1], uint32_t (&o)[C / 4]) {
+                                          const uint32_t (&rc)[C / 2 + 1], uint32_t (&o)[C / 4], uint32_t one) {
     constexpr int NW = C / 2 + 1;
     PfSorted s[NW];
 #pragma unroll
-    for (int k = 0; k < NW; ++k) s[k] = pf_sort3(ra[k], rb[k], rc[k]);
+    for (int k = 0; k < NW; ++k) s[k] = pf_sort3(ra[k], rb[k], rc[k], one);
     uint32_t p[C / 2];
 #pragma unroll
     for (int j = 0; j < C / 2; ++j) {
         const uint32_t lo_m = __byte_perm(s[j].lo, s[j + 1].lo, 0x5432);
         const uint32_t mi_m = __byte_perm(s[j].mi, s[j + 1].mi, 0x5432);
         const uint32_t hi_m = __byte_perm(s[j].hi, s[j + 1].hi, 0x5432);
-        p[j] = pf_med3(__vimax3_u16x2(s[j].lo, lo_m, s[j + 1].lo), pf_med3(s[j].mi, mi_m, s[j + 1].mi),
-                       __vimin3_u16x2(s[j].hi, hi_m, s[j + 1].hi));
+        // med3 of the middles: min / max on the ALU pipe, or (DMSGM_PF_IMAD_MED pairs of the C/2)
+        // the sum minus the extremes with the sums on the FMA pipe (pf_sort3)
+        const uint32_t mm = j < DMSGM_PF_IMAD_MED ? pf_sort3(s[j].mi, mi_m, s[j + 1].mi, one).mi
+                                                  : pf_med3(s[j].mi, mi_m, s[j + 1].mi);
+        p[j] = pf_med3(__vimax3_u16x2(s[j].lo, lo_m, s[j + 1].lo), mm, __vimin3_u16x2(s[j].hi, hi_m, s[j + 1].hi));
     }
 #pragma unroll
     for (int q = 0; q < C / 4; ++q) o[q] = __byte_perm(p[2 * q], p[2 * q + 1], 0x6420);   // 4 columns as bytes
@@ -253,7 +275,7 @@ __device__ __forceinline__ bool pf_row(const PrefilterArgs& a, const PfLane& L, 
         }
         auto emit = [&](int y, const uint32_t (&ra)[NW], const uint32_t (&rb)[NW], const uint32_t (&rc)[NW]) {
             uint32_t o[Q::WPL];
-            pf_median<C>(ra, rb, rc, o);
+            pf_median<C>(ra, rb, rc, o, a.one);
             if (L.writer) {
                 uint8_t* op = L.dst + (long long)y * L.pitch_out;
 #pragma unroll
