@@ -97,7 +97,14 @@ cudaError_t launch_corners(dmsgm_klt_ctx* c, const uint8_t* frames, size_t pitch
     ScoreArgs a;
     a.frames = frames; a.fstride = (long long)c->H * (long long)pitch; a.pitch = (int)pitch;
     a.W = c->W; a.H = c->H; a.cand = c->cand; a.cap = c->cap; a.count = c->cand_count; a.maxbits = c->maxbits;
-    klt_score_kernel<<<dim3((c->W + kTX - 1) / kTX, (c->H + kTY - 1) / kTY, c->S), 256, 0, st>>>(a);
+    if ((c->W & 3) == 0 && (pitch & 3) == 0 && ((uintptr_t)frames & 3) == 0) {
+        // 4-byte aligned rows: the streaming kernel (the same scores and candidates)
+        const int strips = (c->W + 119) / 120;
+        klt_score_stream_kernel<<<dim3((strips + kScoreWarps - 1) / kScoreWarps, (c->H + kScoreBand - 1) / kScoreBand,
+                                       c->S), 32 * kScoreWarps, 0, st>>>(a);
+    } else {
+        klt_score_kernel<<<dim3((c->W + kTX - 1) / kTX, (c->H + kTY - 1) / kTY, c->S), 256, 0, st>>>(a);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     SelectArgs b;
     b.cand = c->cand; b.cap = c->cap; b.count = c->cand_count; b.maxbits = c->maxbits;

@@ -130,6 +130,170 @@ __global__ void __launch_bounds__(256) klt_score_kernel(const ScoreArgs a) {
     }
 }
 
+// Streaming form of K1 for 4-byte aligned frames (W % 4 = 0): a warp walks a vertical strip
+// of 120 columns down kScoreBand rows; lane L holds columns x = xw - 4 + 4L .. x + 3 (lanes 0
+// and 31 are the strip's halo, lanes 1-30 produce).  Per input row r (clamped: the Sobel of
+// replicated pixels, R38): the horizontal Sobel parts dX = p(c+1) - p(c-1) and
+// sX = p(c-1) + 2 p(c) + p(c+1) into a 3-row ring; gradient row g = r - 1, its products
+// Ix^2, IxIy, Iy^2 and their horizontal 3-sums (neighbour columns by shuffles, columns -1 / W
+// replicated) into a 3-row ring (product row -1 / H is row 0 / H-1 again: the oracle pads the
+// products, not the pixels); score row t = r - 2 from the vertical 3-sums (exact integers,
+// fp64 lambda_min, identical to K1); 3x3 local-maximum test of row m = r - 3 against the score
+// ring.  Candidates and the per-stream maximum exactly as K1.  ~8x fewer instructions than K1,
+// whose 32x8 tiles recompute 1.7x the gradients and 1.3x the scores with byte loads.
+constexpr int kScoreBand = 120;
+constexpr int kScoreWarps = 8;
+
+struct ScoreLane {
+    float sl, s0[4], sr;      // a score row: left neighbour column, own 4, right neighbour column
+};
+
+__device__ __forceinline__ float klt_lambda_min(int a, int b, int c) {
+    const double t = (double)(a - c), tb = (double)b;
+    const double d = __fma_rn(t, t, __dmul_rn(4.0 * tb, tb));        // exact: < 2^51
+    return __double2float_rn(__dmul_rn(__dsub_rn((double)(a + c), __dsqrt_rn(d)), 0.5));
+}
+
+__global__ void __launch_bounds__(32 * kScoreWarps) klt_score_stream_kernel(const ScoreArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * kScoreWarps + (threadIdx.x >> 5);
+    const int xw = strip * 120;
+    const int W = a.W, H = a.H;
+    if (xw >= W) return;                                   // warp-uniform
+    const int s = blockIdx.z;
+    const int ys = blockIdx.y * kScoreBand, ye = min(ys + kScoreBand, H);
+    const uint8_t* f = a.frames + (long long)s * a.fstride;
+    const int x = xw - 4 + 4 * lane;
+    const bool mine = lane >= 1 && lane <= 30 && x < W;    // this lane's columns are produced here
+    // clamped word load (columns -4..-1 replicate column 0, columns >= W replicate W-1)
+    const int off = x < 0 ? 0 : (x >= W ? W - 4 : x);
+    const uint32_t sel = x < 0 ? 0x0000u : (x >= W ? 0x3333u : 0x3210u);
+    const bool cl = x == 0, cr = x + 4 == W;               // product columns -1 / W replicated
+    int dX[3][4], sX[3][4];                                // horizontal Sobel parts, rows r mod 3
+    int hxx[3][4], hxy[3][4], hyy[3][4];                   // horizontal 3-sums of the products
+    ScoreLane sc[3];                                       // score rows
+    float smax = 0.0f;
+    const int r0 = ys - 3, r1 = ye + 2;
+    for (int rb = r0; rb <= r1; rb += 3) {
+#pragma unroll
+        for (int ph = 0; ph < 3; ++ph) {
+            const int r = rb + ph;
+            if (r > r1) break;                             // warp-uniform
+            // --- input row r: dX, sX of columns x .. x+3 ---
+            {
+                const uint8_t* row = f + (long long)clampi(r, 0, H - 1) * a.pitch;
+                const uint32_t w = __byte_perm(__ldg(reinterpret_cast<const unsigned int*>(row + off)), 0u, sel);
+                const uint32_t wl = __shfl_up_sync(0xffffffffu, w, 1), wr = __shfl_down_sync(0xffffffffu, w, 1);
+                int p[6];
+                p[0] = (int)(wl >> 24);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) p[k + 1] = (int)((w >> (8 * k)) & 0xFFu);
+                p[5] = (int)(wr & 0xFFu);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    dX[ph][c] = p[c + 2] - p[c];
+                    sX[ph][c] = p[c] + 2 * p[c + 1] + p[c + 2];
+                }
+            }
+            // --- gradient row g = r - 1 (dX / sX rows g-1, g, g+1 = ring slots ph-2, ph-1, ph) ---
+            const int g = r - 1;
+            const int pm1 = (ph + 2) % 3, pm2 = (ph + 1) % 3;
+            if (g >= 0 && g >= ys - 2 && g <= H) {
+                if (g < H) {
+                    int Pxx[4], Pxy[4], Pyy[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int ix = dX[pm2][c] + 2 * dX[pm1][c] + dX[ph][c];
+                        const int iy = sX[ph][c] - sX[pm2][c];
+                        Pxx[c] = ix * ix;
+                        Pxy[c] = ix * iy;
+                        Pyy[c] = iy * iy;
+                    }
+                    int lxx = __shfl_up_sync(0xffffffffu, Pxx[3], 1), rxx = __shfl_down_sync(0xffffffffu, Pxx[0], 1);
+                    int lxy = __shfl_up_sync(0xffffffffu, Pxy[3], 1), rxy = __shfl_down_sync(0xffffffffu, Pxy[0], 1);
+                    int lyy = __shfl_up_sync(0xffffffffu, Pyy[3], 1), ryy = __shfl_down_sync(0xffffffffu, Pyy[0], 1);
+                    if (cl) { lxx = Pxx[0]; lxy = Pxy[0]; lyy = Pyy[0]; }
+                    if (cr) { rxx = Pxx[3]; rxy = Pxy[3]; ryy = Pyy[3]; }
+                    // slot of hs row g: the ring is indexed by the row of the NEXT stage, g -> (ph + 2) % 3
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        hxx[pm1][c] = (c == 0 ? lxx : Pxx[c - 1]) + Pxx[c] + (c == 3 ? rxx : Pxx[c + 1]);
+                        hxy[pm1][c] = (c == 0 ? lxy : Pxy[c - 1]) + Pxy[c] + (c == 3 ? rxy : Pxy[c + 1]);
+                        hyy[pm1][c] = (c == 0 ? lyy : Pyy[c - 1]) + Pyy[c] + (c == 3 ? ryy : Pyy[c + 1]);
+                    }
+                    if (g == 0) {                          // product row -1 := row 0
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            hxx[pm2][c] = hxx[pm1][c]; hxy[pm2][c] = hxy[pm1][c]; hyy[pm2][c] = hyy[pm1][c];
+                        }
+                    }
+                } else {                                   // g == H: product row H := row H-1
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        hxx[pm1][c] = hxx[pm2][c]; hxy[pm1][c] = hxy[pm2][c]; hyy[pm1][c] = hyy[pm2][c];
+                    }
+                }
+            }
+            // --- score row t = r - 2 (hs rows t-1, t, t+1 = slots ph, ph+1, ph+2 of the hs ring:
+            //     hs row q sits in slot (q + 1 - r0) mod 3 ... i.e. rows t-1 / t / t+1 in pm2 / ph / pm1) ---
+            const int t = r - 2;
+            if (t >= max(ys - 1, 0) && t <= min(ye, H - 1)) {
+                ScoreLane& S = sc[ph];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int sa = hxx[pm2][c] + hxx[ph][c] + hxx[pm1][c];
+                    const int sb = hxy[pm2][c] + hxy[ph][c] + hxy[pm1][c];
+                    const int scc = hyy[pm2][c] + hyy[ph][c] + hyy[pm1][c];
+                    S.s0[c] = klt_lambda_min(sa, sb, scc);
+                    if (mine && t >= ys && t < ye && x + c < W) smax = fmaxf(smax, S.s0[c]);
+                }
+                S.sl = __shfl_up_sync(0xffffffffu, S.s0[3], 1);
+                S.sr = __shfl_down_sync(0xffffffffu, S.s0[0], 1);
+            }
+            // --- local maxima of row m = r - 3 (score rows m-1, m, m+1 = slots ph-2, ph-1, ph) ---
+            const int m = r - 3;
+            if (m >= max(ys, 1) && m <= min(ye - 1, H - 2)) {
+                const ScoreLane& U = sc[pm2];
+                const ScoreLane& C = sc[pm1];
+                const ScoreLane& D = sc[ph];
+                bool cand[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float v = C.s0[c];
+                    const float ul = c == 0 ? U.sl : U.s0[c - 1], ur = c == 3 ? U.sr : U.s0[c + 1];
+                    const float cl_ = c == 0 ? C.sl : C.s0[c - 1], cr_ = c == 3 ? C.sr : C.s0[c + 1];
+                    const float dl = c == 0 ? D.sl : D.s0[c - 1], dr = c == 3 ? D.sr : D.s0[c + 1];
+                    const float nb = fmaxf(fmaxf(fmaxf(ul, U.s0[c]), fmaxf(ur, cl_)), fmaxf(fmaxf(cr_, dl), fmaxf(D.s0[c], dr)));
+                    const int xc = x + c;
+                    cand[c] = mine && xc >= 1 && xc < W - 1 && v > 0.0f && v >= nb;
+                }
+                // warp-aggregated append (every lane takes part: cand is false where not mine)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const unsigned bal = __ballot_sync(0xffffffffu, cand[c]);
+                    if (bal) {
+                        unsigned base = 0;
+                        if (lane == 0) base = atomicAdd(a.count + s, (unsigned)__popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (cand[c]) {
+                            const unsigned pos = base + __popc(bal & ((1u << lane) - 1u));
+                            const unsigned idx = (unsigned)(m * W + x + c);
+                            if (pos < (unsigned)a.cap)
+                                a.cand[(long long)s * a.cap + pos] =
+                                    ((unsigned long long)__float_as_uint(C.s0[c]) << 32) |
+                                    (unsigned long long)(0xFFFFFFFFu - idx);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    // per-stream max over every pixel (scores >= +0: bits order like values)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    if (lane == 0) atomicMax(a.maxbits + s, __float_as_uint(smax));
+}
+
 // ---------------------------------------------------------------------------------------
 // K2: quality threshold, exact top-kBatch radix select, bitonic sort, greedy min-distance
 // ---------------------------------------------------------------------------------------
@@ -364,10 +528,27 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// Pixel (x, y) of a level image as a float, border pixels repeated (R40's bilinear rule).
+__device__ __forceinline__ float pix_clamped(const uint8_t* img, int pitch, int w, int h, int x, int y) {
+    return (float)__ldg(img + (long long)clampi(y, 0, h - 1) * pitch + clampi(x, 0, w - 1));
+}
+
+// One warp per corner (R40).  The window's samples s = p_L + (i - half, j - half) all share
+// the fractional part of p_L (p_L = c / 2^L and the offsets are exact in fp32), so on
+// prev the bilinear values of the (win+2)^2 integer-offset grid around the window are
+// computed once per level into shared memory with common weights -- bitwise the values
+// bil() gives at every sample and at its +-1 neighbours -- and I, Ix, Iy are read from it.
+// On next, each iteration's samples s + g + v likewise share one fractional offset (the
+// guess is added to the window's base point once), so a sample is 4 byte loads and the
+// blend with common weights; windows wholly inside the level image skip the clamps.
+constexpr int kLkWarps = 8;
+constexpr int kLkMaxWin = 32;
+
 template <int NS>   // samples per lane: ceil(win^2 / 32)
-__global__ void __launch_bounds__(256) klt_lk_kernel(const LkArgs a) {
+__global__ void __launch_bounds__(32 * kLkWarps) klt_lk_kernel(const LkArgs a) {
+    __shared__ float patch_all[kLkWarps][(kLkMaxWin + 2) * (kLkMaxWin + 2)];
     const int lane = threadIdx.x & 31;
-    const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int i = blockIdx.x * kLkWarps + (threadIdx.x >> 5);
     const int s = blockIdx.y;
     if (i >= a.max_corners) return;
     const long long o = (long long)s * a.max_corners + i;
@@ -379,9 +560,18 @@ __global__ void __launch_bounds__(256) klt_lk_kernel(const LkArgs a) {
         }
         return;
     }
+    float* patch = patch_all[threadIdx.x >> 5];
     const float cx = (float)a.corners[2 * o] + 0.5f, cy = (float)a.corners[2 * o + 1] + 0.5f;
-    const int win = a.win, nsamp = win * win;
+    const int win = a.win, nsamp = win * win, pw = win + 2;
     const float half = 0.5f * (float)(win - 1);
+    // sample q = lane + 32 k of the window, (ii, jj) = (q % win, q / win): its patch index
+    // (constant) and its byte offset in the level image (per level)
+    int pidx[NS], boff[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const int q = lane + 32 * k, jj = q / win;
+        pidx[k] = (jj + 1) * pw + (q - jj * win) + 1;
+    }
     float gx = 0.0f, gy = 0.0f;
     bool ok = true;
     for (int L = a.nlev - 1; L >= 0 && ok; --L) {
@@ -390,22 +580,44 @@ __global__ void __launch_bounds__(256) klt_lk_kernel(const LkArgs a) {
         const uint8_t* qp = Q.p + (long long)s * Q.stride;
         const float sc = __int_as_float((127 - L) << 23);        // 2^-L
         const float plx = __fmul_rn(cx, sc), ply = __fmul_rn(cy, sc);
-        float I[NS], Ix[NS], Iy[NS], sx[NS], sy[NS];
+        // window sample (ii, jj) sits at u = p_L - half - 0.5 + ii (+ the guess on next):
+        // floor / fraction of the base point once (exact: p_L and the offsets are short)
+        {
+            const float ux = __fsub_rn(__fadd_rn(plx, __fsub_rn(0.0f, half)), 0.5f);
+            const float uy = __fsub_rn(__fadd_rn(ply, __fsub_rn(0.0f, half)), 0.5f);
+            const float xf = floorf(ux), yf = floorf(uy);
+            const float fx = __fsub_rn(ux, xf), fy = __fsub_rn(uy, yf);
+            const float gxw = __fsub_rn(1.0f, fx), gyw = __fsub_rn(1.0f, fy);
+            const int X0 = (int)xf, Y0 = (int)yf;
+            // patch[(jj + 1) * pw + (ii + 1)] = bil(prev, sample (ii, jj)), ii, jj in [-1, win]
+            __syncwarp();
+            for (int q = lane; q < pw * pw; q += 32) {
+                const int jj = q / pw - 1, ii = q - (jj + 1) * pw - 1;
+                const int x = X0 + ii, y = Y0 + jj;
+                const float p00 = pix_clamped(pp, P.pitch, P.w, P.h, x, y), p10 = pix_clamped(pp, P.pitch, P.w, P.h, x + 1, y);
+                const float p01 = pix_clamped(pp, P.pitch, P.w, P.h, x, y + 1),
+                            p11 = pix_clamped(pp, P.pitch, P.w, P.h, x + 1, y + 1);
+                const float top = __fadd_rn(__fmul_rn(p00, gxw), __fmul_rn(p10, fx));
+                const float bot = __fadd_rn(__fmul_rn(p01, gxw), __fmul_rn(p11, fx));
+                patch[q] = __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy));
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const int q = lane + 32 * k, jj = q / win;
+            boff[k] = jj * Q.pitch + (q - jj * win);
+        }
+        float I[NS], Ix[NS], Iy[NS];
         float gxx = 0.0f, gxy = 0.0f, gyy = 0.0f;
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
-            const int q = lane + 32 * k;
             I[k] = Ix[k] = Iy[k] = 0.0f;
-            sx[k] = sy[k] = 0.0f;
-            if (q < nsamp) {
-                const int jj = q / win, ii = q - jj * win;
-                sx[k] = __fadd_rn(plx, __fsub_rn((float)ii, half));
-                sy[k] = __fadd_rn(ply, __fsub_rn((float)jj, half));
-                I[k] = bil(pp, P.pitch, P.w, P.h, sx[k], sy[k]);
-                Ix[k] = __fmul_rn(__fsub_rn(bil(pp, P.pitch, P.w, P.h, __fadd_rn(sx[k], 1.0f), sy[k]),
-                                            bil(pp, P.pitch, P.w, P.h, __fsub_rn(sx[k], 1.0f), sy[k])), 0.5f);
-                Iy[k] = __fmul_rn(__fsub_rn(bil(pp, P.pitch, P.w, P.h, sx[k], __fadd_rn(sy[k], 1.0f)),
-                                            bil(pp, P.pitch, P.w, P.h, sx[k], __fsub_rn(sy[k], 1.0f))), 0.5f);
+            if (lane + 32 * k < nsamp) {
+                const float* c0 = patch + pidx[k];
+                I[k] = c0[0];
+                Ix[k] = __fmul_rn(__fsub_rn(c0[1], c0[-1]), 0.5f);
+                Iy[k] = __fmul_rn(__fsub_rn(c0[pw], c0[-pw]), 0.5f);
                 gxx = __fadd_rn(gxx, __fmul_rn(Ix[k], Ix[k]));
                 gxy = __fadd_rn(gxy, __fmul_rn(Ix[k], Iy[k]));
                 gyy = __fadd_rn(gyy, __fmul_rn(Iy[k], Iy[k]));
@@ -429,12 +641,42 @@ __global__ void __launch_bounds__(256) klt_lk_kernel(const LkArgs a) {
         for (int it = 0; it < a.max_iters; ++it) {
             float bx = 0.0f, by = 0.0f;
             const float ox = __fadd_rn(gx, vx), oy = __fadd_rn(gy, vy);
+            // the iteration's window on next: base point, its floor and common fraction
+            const float ux = __fsub_rn(__fadd_rn(__fadd_rn(plx, ox), __fsub_rn(0.0f, half)), 0.5f);
+            const float uy = __fsub_rn(__fadd_rn(__fadd_rn(ply, oy), __fsub_rn(0.0f, half)), 0.5f);
+            const float xf = floorf(ux), yf = floorf(uy);
+            const float fx = __fsub_rn(ux, xf), fy = __fsub_rn(uy, yf);
+            const float gxw = __fsub_rn(1.0f, fx), gyw = __fsub_rn(1.0f, fy);
+            const int X0 = (int)xf, Y0 = (int)yf;
+            if (X0 >= 0 && Y0 >= 0 && X0 + win < Q.w && Y0 + win < Q.h) {
+                // the window and its +1 neighbours inside the level: no clamps
+                const uint8_t* base = qp + (long long)Y0 * Q.pitch + X0;
 #pragma unroll
-            for (int k = 0; k < NS; ++k) {
-                if (lane + 32 * k < nsamp) {
-                    const float e = __fsub_rn(I[k], bil(qp, Q.pitch, Q.w, Q.h, __fadd_rn(sx[k], ox), __fadd_rn(sy[k], oy)));
-                    bx = __fadd_rn(bx, __fmul_rn(e, Ix[k]));
-                    by = __fadd_rn(by, __fmul_rn(e, Iy[k]));
+                for (int k = 0; k < NS; ++k) {
+                    if (lane + 32 * k < nsamp) {
+                        const uint8_t* r0 = base + boff[k];
+                        const uint8_t* r1 = r0 + Q.pitch;
+                        const float top = __fadd_rn(__fmul_rn((float)__ldg(r0), gxw), __fmul_rn((float)__ldg(r0 + 1), fx));
+                        const float bot = __fadd_rn(__fmul_rn((float)__ldg(r1), gxw), __fmul_rn((float)__ldg(r1 + 1), fx));
+                        const float e = __fsub_rn(I[k], __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy)));
+                        bx = __fadd_rn(bx, __fmul_rn(e, Ix[k]));
+                        by = __fadd_rn(by, __fmul_rn(e, Iy[k]));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                    if (lane + 32 * k < nsamp) {
+                        const int q = lane + 32 * k, jj = q / win;
+                        const int x = X0 + (q - jj * win), y = Y0 + jj;
+                        const float top = __fadd_rn(__fmul_rn(pix_clamped(qp, Q.pitch, Q.w, Q.h, x, y), gxw),
+                                                    __fmul_rn(pix_clamped(qp, Q.pitch, Q.w, Q.h, x + 1, y), fx));
+                        const float bot = __fadd_rn(__fmul_rn(pix_clamped(qp, Q.pitch, Q.w, Q.h, x, y + 1), gxw),
+                                                    __fmul_rn(pix_clamped(qp, Q.pitch, Q.w, Q.h, x + 1, y + 1), fx));
+                        const float e = __fsub_rn(I[k], __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy)));
+                        bx = __fadd_rn(bx, __fmul_rn(e, Ix[k]));
+                        by = __fadd_rn(by, __fmul_rn(e, Iy[k]));
+                    }
                 }
             }
             bx = warp_sum(bx);
