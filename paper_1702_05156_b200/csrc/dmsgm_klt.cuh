@@ -18,6 +18,7 @@
 //                       the smallest eigenvector of A^T A (cyclic Jacobi, fp64) (R41)
 #pragma once
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <stdint.h>
 
 namespace dmsgm_klt {
@@ -142,6 +143,8 @@ __global__ void __launch_bounds__(256) klt_score_kernel(const ScoreArgs a) {
 // ring.  Candidates and the per-stream maximum exactly as K1.  ~8x fewer instructions than K1,
 // whose 32x8 tiles recompute 1.7x the gradients and 1.3x the scores with byte loads.
 constexpr int kScoreBand = 120;
+constexpr int kScorePrefetch = 8;
+constexpr int kCbuf = 384;          // per-warp candidate buffer (keys): flushed above kCbuf - 128
 constexpr int kScoreWarps = 8;
 
 struct ScoreLane {
@@ -173,6 +176,21 @@ __global__ void __launch_bounds__(32 * kScoreWarps) klt_score_stream_kernel(cons
     int hxx[3][4], hxy[3][4], hyy[3][4];                   // horizontal 3-sums of the products
     ScoreLane sc[3];                                       // score rows
     float smax = 0.0f;
+    // candidate keys of this warp, flushed to the stream's list in blocks
+    __shared__ unsigned long long cbuf_all[kScoreWarps][kCbuf];
+    unsigned long long* cbuf = cbuf_all[threadIdx.x >> 5];
+    int nbuf = 0;                                          // (warp-uniform)
+    auto flush = [&]() {
+        __syncwarp();
+        if (nbuf == 0) return;
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(a.count + s, (unsigned)nbuf);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int i = lane; i < nbuf; i += 32)
+            if (base + i < (unsigned)a.cap) a.cand[(long long)s * a.cap + base + i] = cbuf[i];
+        __syncwarp();
+        nbuf = 0;
+    };
     const int r0 = ys - 3, r1 = ye + 2;
     for (int rb = r0; rb <= r1; rb += 3) {
 #pragma unroll
@@ -182,6 +200,8 @@ __global__ void __launch_bounds__(32 * kScoreWarps) klt_score_stream_kernel(cons
             // --- input row r: dX, sX of columns x .. x+3 ---
             {
                 const uint8_t* row = f + (long long)clampi(r, 0, H - 1) * a.pitch;
+                // the row kScorePrefetch ahead into L1: this row's load then waits ~L1, not HBM
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(f + (long long)clampi(r + kScorePrefetch, 0, H - 1) * a.pitch + off));
                 const uint32_t w = __byte_perm(__ldg(reinterpret_cast<const unsigned int*>(row + off)), 0u, sel);
                 const uint32_t wl = __shfl_up_sync(0xffffffffu, w, 1), wr = __shfl_down_sync(0xffffffffu, w, 1);
                 int p[6];
@@ -267,27 +287,24 @@ __global__ void __launch_bounds__(32 * kScoreWarps) klt_score_stream_kernel(cons
                     const int xc = x + c;
                     cand[c] = mine && xc >= 1 && xc < W - 1 && v > 0.0f && v >= nb;
                 }
-                // warp-aggregated append (every lane takes part: cand is false where not mine)
+                // append to the warp's shared-memory buffer (every lane takes part: cand is
+                // false where not mine); the buffer goes to the stream's list by one atomic
+                // per flush (an atomic per ballot left the warp waiting on its round trip)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const unsigned bal = __ballot_sync(0xffffffffu, cand[c]);
-                    if (bal) {
-                        unsigned base = 0;
-                        if (lane == 0) base = atomicAdd(a.count + s, (unsigned)__popc(bal));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        if (cand[c]) {
-                            const unsigned pos = base + __popc(bal & ((1u << lane) - 1u));
-                            const unsigned idx = (unsigned)(m * W + x + c);
-                            if (pos < (unsigned)a.cap)
-                                a.cand[(long long)s * a.cap + pos] =
-                                    ((unsigned long long)__float_as_uint(C.s0[c]) << 32) |
-                                    (unsigned long long)(0xFFFFFFFFu - idx);
-                        }
+                    if (cand[c]) {
+                        const unsigned idx = (unsigned)(m * W + x + c);
+                        cbuf[nbuf + __popc(bal & ((1u << lane) - 1u))] =
+                            ((unsigned long long)__float_as_uint(C.s0[c]) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
                     }
+                    nbuf += __popc(bal);
                 }
+                if (nbuf > kCbuf - 128) flush();
             }
         }
     }
+    flush();
     // per-stream max over every pixel (scores >= +0: bits order like values)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
@@ -544,9 +561,15 @@ __device__ __forceinline__ float pix_clamped(const uint8_t* img, int pitch, int 
 constexpr int kLkWarps = 8;
 constexpr int kLkMaxWin = 32;
 
+constexpr int kLkMargin = 4;     // next-image region: the window +- this many pixels of flow per level
+
 template <int NS>   // samples per lane: ceil(win^2 / 32)
-__global__ void __launch_bounds__(32 * kLkWarps) klt_lk_kernel(const LkArgs a) {
-    __shared__ float patch_all[kLkWarps][(kLkMaxWin + 2) * (kLkMaxWin + 2)];
+__global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? 3 : 1) klt_lk_kernel(const LkArgs a) {
+    constexpr int MW = NS <= 8 ? 16 : (NS <= 13 ? 20 : kLkMaxWin);   // largest window of this variant
+    constexpr bool STAGE = NS <= 13;       // (win > 20: the regions would exceed 48 KB; global reads)
+    constexpr int MR = STAGE ? MW + 1 + 2 * kLkMargin : 1;             // next-region side
+    __shared__ float patch_all[kLkWarps][(MW + 2) * (MW + 2)];
+    __shared__ float region_all[kLkWarps][MR * MR];
     const int lane = threadIdx.x & 31;
     const int i = blockIdx.x * kLkWarps + (threadIdx.x >> 5);
     const int s = blockIdx.y;
@@ -561,16 +584,17 @@ __global__ void __launch_bounds__(32 * kLkWarps) klt_lk_kernel(const LkArgs a) {
         return;
     }
     float* patch = patch_all[threadIdx.x >> 5];
+    float* region = region_all[threadIdx.x >> 5];
     const float cx = (float)a.corners[2 * o] + 0.5f, cy = (float)a.corners[2 * o + 1] + 0.5f;
-    const int win = a.win, nsamp = win * win, pw = win + 2;
+    const int win = a.win, nsamp = win * win, pw = win + 2, rs = win + 1 + 2 * kLkMargin;
     const float half = 0.5f * (float)(win - 1);
-    // sample q = lane + 32 k of the window, (ii, jj) = (q % win, q / win): its patch index
-    // (constant) and its byte offset in the level image (per level)
-    int pidx[NS], boff[NS];
+    // sample q = lane + 32 k of the window, (ii, jj) = (q % win, q / win): its offset in the
+    // next-image region
+    int roff[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         const int q = lane + 32 * k, jj = q / win;
-        pidx[k] = (jj + 1) * pw + (q - jj * win) + 1;
+        roff[k] = jj * rs + (q - jj * win);
     }
     float gx = 0.0f, gy = 0.0f;
     bool ok = true;
@@ -591,6 +615,7 @@ __global__ void __launch_bounds__(32 * kLkWarps) klt_lk_kernel(const LkArgs a) {
             const int X0 = (int)xf, Y0 = (int)yf;
             // patch[(jj + 1) * pw + (ii + 1)] = bil(prev, sample (ii, jj)), ii, jj in [-1, win]
             __syncwarp();
+#pragma unroll 4
             for (int q = lane; q < pw * pw; q += 32) {
                 const int jj = q / pw - 1, ii = q - (jj + 1) * pw - 1;
                 const int x = X0 + ii, y = Y0 + jj;
@@ -603,10 +628,22 @@ __global__ void __launch_bounds__(32 * kLkWarps) klt_lk_kernel(const LkArgs a) {
             }
             __syncwarp();
         }
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            const int q = lane + 32 * k, jj = q / win;
-            boff[k] = jj * Q.pitch + (q - jj * win);
+        // the next-image region of this level: the window at the level's initial guess,
+        // +- kLkMargin pixels, as floats in shared memory (clamped, R40's border rule); the
+        // iterations read it while their window stays inside
+        int RX0, RY0;
+        {
+            const float ux = __fsub_rn(__fadd_rn(__fadd_rn(plx, gx), __fsub_rn(0.0f, half)), 0.5f);
+            const float uy = __fsub_rn(__fadd_rn(__fadd_rn(ply, gy), __fsub_rn(0.0f, half)), 0.5f);
+            RX0 = STAGE ? (int)floorf(ux) - kLkMargin : INT_MIN / 2;      // INT_MIN / 2: never inside
+            RY0 = (int)floorf(uy) - kLkMargin;
+            __syncwarp();
+#pragma unroll 4
+            for (int q = lane; STAGE && q < rs * rs; q += 32) {
+                const int jj = q / rs, ii = q - jj * rs;
+                region[q] = pix_clamped(qp, Q.pitch, Q.w, Q.h, RX0 + ii, RY0 + jj);
+            }
+            __syncwarp();
         }
         float I[NS], Ix[NS], Iy[NS];
         float gxx = 0.0f, gxy = 0.0f, gyy = 0.0f;
@@ -614,7 +651,8 @@ __global__ void __launch_bounds__(32 * kLkWarps) klt_lk_kernel(const LkArgs a) {
         for (int k = 0; k < NS; ++k) {
             I[k] = Ix[k] = Iy[k] = 0.0f;
             if (lane + 32 * k < nsamp) {
-                const float* c0 = patch + pidx[k];
+                const int q = lane + 32 * k, jj = q / win;
+                const float* c0 = patch + (jj + 1) * pw + (q - jj * win) + 1;
                 I[k] = c0[0];
                 Ix[k] = __fmul_rn(__fsub_rn(c0[1], c0[-1]), 0.5f);
                 Iy[k] = __fmul_rn(__fsub_rn(c0[pw], c0[-pw]), 0.5f);
@@ -648,16 +686,17 @@ __global__ void __launch_bounds__(32 * kLkWarps) klt_lk_kernel(const LkArgs a) {
             const float fx = __fsub_rn(ux, xf), fy = __fsub_rn(uy, yf);
             const float gxw = __fsub_rn(1.0f, fx), gyw = __fsub_rn(1.0f, fy);
             const int X0 = (int)xf, Y0 = (int)yf;
-            if (X0 >= 0 && Y0 >= 0 && X0 + win < Q.w && Y0 + win < Q.h) {
-                // the window and its +1 neighbours inside the level: no clamps
-                const uint8_t* base = qp + (long long)Y0 * Q.pitch + X0;
+            const int dxr = X0 - RX0, dyr = Y0 - RY0;
+            if ((unsigned)dxr <= 2u * kLkMargin && (unsigned)dyr <= 2u * kLkMargin) {
+                // the window (and its +1 neighbours) inside the staged region
+                const float* base = region + dyr * rs + dxr;
 #pragma unroll
                 for (int k = 0; k < NS; ++k) {
                     if (lane + 32 * k < nsamp) {
-                        const uint8_t* r0 = base + boff[k];
-                        const uint8_t* r1 = r0 + Q.pitch;
-                        const float top = __fadd_rn(__fmul_rn((float)__ldg(r0), gxw), __fmul_rn((float)__ldg(r0 + 1), fx));
-                        const float bot = __fadd_rn(__fmul_rn((float)__ldg(r1), gxw), __fmul_rn((float)__ldg(r1 + 1), fx));
+                        const float* r0 = base + roff[k];
+                        const float p00 = r0[0], p10 = r0[1], p01 = r0[rs], p11 = r0[rs + 1];
+                        const float top = __fadd_rn(__fmul_rn(p00, gxw), __fmul_rn(p10, fx));
+                        const float bot = __fadd_rn(__fmul_rn(p01, gxw), __fmul_rn(p11, fx));
                         const float e = __fsub_rn(I[k], __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy)));
                         bx = __fadd_rn(bx, __fmul_rn(e, Ix[k]));
                         by = __fadd_rn(by, __fmul_rn(e, Iy[k]));
