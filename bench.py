@@ -356,6 +356,13 @@ def run_dmsgm(args, rank, world, local):
         ctx.set_prefilter(*pf)                  # Gaussian + median before the step
     if args.motion == "frame":
         ctx.set_motion(dm.DMSGM_MC_FRAME)       # App. F frame warp, models not warped
+    klt = None
+    if args.motion == "estimate":
+        # the homographies are estimated on the GPU from the frames
+        # (App. F: corners -> pyramidal LK -> RANSAC), then drive the step -- closed loop
+        klt = dm.Klt(W, H, dm.KltParams(num_streams=S), device=local)
+        H_est = torch.zeros((S, 9), dtype=torch.float64, device=dev)
+        args.launch = "step"                    # 7 estimation launches + the step per frame, no graph
     info = ctx.info
     stream = torch.cuda.current_stream(dev)
     bytes_per_step = S * info.algorithmic_bytes_per_frame
@@ -368,7 +375,11 @@ def run_dmsgm(args, rank, world, local):
     chunks = [GRAPH_T] * (args.steps // GRAPH_T) + ([args.steps % GRAPH_T] if args.steps % GRAPH_T else [])
 
     def replay(T):
-        if args.launch == "graph":
+        if klt is not None:                     # estimate H_t from frames t-1, t; step frame t with it
+            for i in range(T):
+                klt.estimate(frames[(i - 1) % GRAPH_T], frames[i], H_est, stream=stream)
+                ctx.step(frames[i], H_est, masks[i], stream)
+        elif args.launch == "graph":
             ctx.step_n(T, frames[:T], Hs_dev[:T], masks[:T], stream)
         else:                                   # A/B: T single dmsgm_step launches
             for i in range(T):
@@ -416,7 +427,7 @@ def run_dmsgm(args, rank, world, local):
 
     # ---- end to end through the public API with HOST buffers (pinned) ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and klt is None:
         hf = torch.empty((S, H, W), dtype=torch.uint8, pin_memory=True)
         hm = torch.empty((S, H, W), dtype=torch.uint8, pin_memory=True)
         hH = torch.empty((RING, S, 9), dtype=torch.float64, pin_memory=True)
@@ -511,6 +522,29 @@ def run_dmsgm(args, rank, world, local):
                                   2.0 * S * W * H, None, w_ms / ms_per_step,
                                   "profiles/ncu_instr_warp_C4.json (scaled by pixels for other workloads)")
         warp_roof["peak_source"] = peak_src
+    klt_roof = None
+    if klt is not None:
+        # the estimation alone (CUDA events on the launching stream): HBM view of its
+        # algorithmic bytes (both frames read, 2 B/px; the pyramid and candidate traffic is
+        # not algorithmic) and the measured instruction rate from the committed launch list
+        for i in range(3):
+            klt.estimate(frames[i], frames[i + 1], H_est, stream=stream)
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kk = max(5, min(args.steps, 20))
+        p0.record(stream)
+        for i in range(kk):
+            klt.estimate(frames[i % 39], frames[i % 39 + 1], H_est, stream=stream)
+        p1.record(stream)
+        p1.synchronize()
+        k_ms = p0.elapsed_time(p1) / kk
+        kbytes = 2.0 * S * W * H
+        klt_roof = {"bound": "hbm", "achieved": kbytes / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": kbytes / (k_ms * 1e-3) / 1e9 / peak, "traffic": None,
+                    "algorithmic_bytes_per_launch": kbytes, "kernel": "dmsgm_klt_estimate (7 kernels)",
+                    "ms_per_launch": k_ms, "share_of_step": k_ms / ms_per_step,
+                    "kernels": "profiles/R2_klt_launches.md (per-kernel split; LK, radix select and score lead)",
+                    "peak_source": peak_src}
+        klt.close()
     kernel_name = info.kernel.decode()
     ctx.close()
     if rank == 0:
@@ -528,8 +562,8 @@ def run_dmsgm(args, rank, world, local):
                       f"median_ms_per_step = median over the {len(rep_ms)} full replays",
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth/ ring recipe, generated on device)",
-            "config": {"workload": args.config + ("+prefilter" if pf else "") + ("+framewarp" if args.motion == "frame"
-                                                                                   else ""),
+            "config": {"workload": args.config + ("+prefilter" if pf else "") +
+                                   {"frame": "+framewarp", "estimate": "+klt"}.get(args.motion, ""),
                        "desc": wl["desc"], "W": W, "H": H, "motion_compensation": args.motion,
                        "N": N, "prefilter": {"gauss_size": pf[0], "gauss_sigma": pf[1], "median_radius": pf[2]}
                        if pf else None,
@@ -554,7 +588,7 @@ def run_dmsgm(args, rank, world, local):
         # with preprocessing and/or frame warping the dominant kernel of the step can be the
         # (ALU-bound) filter or warp kernel: if one takes half the step or more it becomes
         # `roofline` and the HBM figure of the whole step is kept as roofline_step
-        extra = [r for r in (pf_roof, warp_roof) if r]
+        extra = [r for r in (pf_roof, warp_roof, klt_roof) if r]
         if extra and max(r["share_of_step"] for r in extra) >= 0.5:
             line["roofline_step"] = line["roofline"]
             line["roofline"] = max(extra, key=lambda r: r["share_of_step"])
@@ -562,6 +596,8 @@ def run_dmsgm(args, rank, world, local):
             line["roofline_prefilter"] = pf_roof
         if warp_roof:
             line["roofline_warp"] = warp_roof
+        if klt_roof:
+            line["roofline_klt"] = klt_roof
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -791,7 +827,7 @@ def main():
                     help="C5b under torchrun: fused peer stores + sync kernel, or NCCL send/recv baseline")
     ap.add_argument("--prefilter", default="",
                     help="GAUSS_SIZE,SIGMA,MEDIAN_RADIUS (e.g. 5,1.0,1): NEXT-2 preprocessing before every step")
-    ap.add_argument("--motion", default="models", choices=["models", "frame"],
+    ap.add_argument("--motion", default="models", choices=["models", "frame", "estimate"],
                     help="motion compensation: warp the models (default, north_star) or the frame (App. F, NEXT-3)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo + --same-device: functional test of the torchrun path on one GPU)")
