@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
+#include <functional>
 #include <stdio.h>
 #include <string.h>
 
@@ -42,6 +43,10 @@ struct dmsgm_klt_ctx {
     double* dst;
     int* mcount;                     // [S]
     int* iter_counts;                // [S][iters]
+    // dmsgm_klt_estimate forks the pyramid (which needs only the frames) onto `side`, beside
+    // the corner score / select kernels, and joins before LK
+    cudaStream_t side;
+    cudaEvent_t ev_fork, ev_pyr;
     char err[512];
 };
 
@@ -91,7 +96,7 @@ bool params_ok(const dmsgm_klt_params* p, char* why, size_t n) {
 bool img_ok(const dmsgm_klt_ctx* c, const void* p, size_t pitch) { return p && pitch >= (size_t)c->W; }
 
 cudaError_t launch_corners(dmsgm_klt_ctx* c, const uint8_t* frames, size_t pitch, int* corners, int* counts,
-                           cudaStream_t st) {
+                           cudaStream_t st, const std::function<cudaError_t()>& after_score = nullptr) {
     cudaError_t e = cudaMemsetAsync(c->cand_count, 0, 2 * c->S * sizeof(unsigned), st);   // counts + maxbits
     if (e != cudaSuccess) return e;
     ScoreArgs a;
@@ -106,6 +111,7 @@ cudaError_t launch_corners(dmsgm_klt_ctx* c, const uint8_t* frames, size_t pitch
         klt_score_kernel<<<dim3((c->W + kTX - 1) / kTX, (c->H + kTY - 1) / kTY, c->S), 256, 0, st>>>(a);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (after_score && (e = after_score()) != cudaSuccess) return e;
     SelectArgs b;
     b.cand = c->cand; b.cap = c->cap; b.count = c->cand_count; b.maxbits = c->maxbits;
     b.quality = c->p.quality; b.min_dist2 = c->p.min_distance * c->p.min_distance;
@@ -117,7 +123,8 @@ cudaError_t launch_corners(dmsgm_klt_ctx* c, const uint8_t* frames, size_t pitch
 }
 
 cudaError_t launch_track(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, const uint8_t* next, size_t npitch,
-                         const int* corners, const int* counts, float* tracked, uint8_t* status, cudaStream_t st) {
+                         const int* corners, const int* counts, float* tracked, uint8_t* status, cudaStream_t st,
+                         bool skip_pyramid = false) {
     cudaError_t e;
     PyrArgs pa;
     pa.img0[0] = prev; pa.img0[1] = next;
@@ -125,7 +132,7 @@ cudaError_t launch_track(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, c
     pa.pitch0[0] = (int)ppitch; pa.pitch0[1] = (int)npitch;
     for (int L = 0; L < kMaxLevels; ++L) { pa.lev[L] = c->pyr[L]; pa.w[L] = c->lw[L]; pa.h[L] = c->lh[L]; }
     pa.nlev = c->nlev; pa.S = c->S;
-    if (c->nlev > 1) {
+    if (c->nlev > 1 && !skip_pyramid) {
         klt_pyramid_kernel<<<dim3((c->lw[1] + 15) / 16, (c->lh[1] + 15) / 16, 2 * c->S), 256, 0, st>>>(pa);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
@@ -198,7 +205,7 @@ int dmsgm_klt_create(int width, int height, const dmsgm_klt_params* p, int devic
     if (c->cell < 1) c->cell = 1;
     c->gw = (width + c->cell - 1) / c->cell;
     c->gh = (height + c->cell - 1) / c->cell;
-    const size_t base_smem = (size_t)kBatch * 8 + 256 * 4 + (size_t)kMaxCorners * 8;
+    const size_t base_smem = (size_t)kBatch * 8 + 256 * 4 + (size_t)kMaxCorners * 8 + (size_t)kBatch * 8;
     const size_t grid_bytes = (size_t)c->gw * c->gh * 2;
     const bool grid_in_smem = base_smem + grid_bytes <= 200 * 1024;
     c->sel_smem = base_smem + (grid_in_smem ? grid_bytes : 0);
@@ -220,6 +227,9 @@ int dmsgm_klt_create(int width, int height, const dmsgm_klt_params* p, int devic
     if (!grid_in_smem) KALLOC(c->grid_global, (size_t)S * grid_bytes);
     for (int L = 1; L < c->nlev; ++L) KALLOC(c->pyr[L], 2 * (size_t)S * c->lw[L] * c->lh[L]);
 #undef KALLOC
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_pyr, cudaEventDisableTiming);
     if (e == cudaSuccess) c->maxbits = c->cand_count + S;
     if (e == cudaSuccess) e = cudaMemset(c->overflow, 0, sizeof(unsigned));
     if (e == cudaSuccess)
@@ -274,8 +284,28 @@ int dmsgm_klt_estimate(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, con
         return kfail(c, DMSGM_EINVAL, "bad frames / outputs");
     Dev g(c->device);
     cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = launch_corners(c, prev, ppitch, c->corners, c->counts, st);
-    if (e == cudaSuccess) e = launch_track(c, prev, ppitch, next, npitch, c->corners, c->counts, c->tracked, c->status, st);
+    cudaError_t e = cudaSuccess;
+    // the pyramid of prev and next on the side stream, forked after the score kernel so that it
+    // runs beside the select kernel (32 CTAs: most SMs idle); joined before LK
+    auto fork_pyramid = [&]() -> cudaError_t {
+        if (c->nlev <= 1) return cudaSuccess;
+        cudaError_t fe = cudaEventRecord(c->ev_fork, st);
+        if (fe == cudaSuccess) fe = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+        if (fe != cudaSuccess) return fe;
+        PyrArgs pa;
+        pa.img0[0] = prev; pa.img0[1] = next;
+        pa.stride0[0] = (long long)c->H * (long long)ppitch; pa.stride0[1] = (long long)c->H * (long long)npitch;
+        pa.pitch0[0] = (int)ppitch; pa.pitch0[1] = (int)npitch;
+        for (int L = 0; L < kMaxLevels; ++L) { pa.lev[L] = c->pyr[L]; pa.w[L] = c->lw[L]; pa.h[L] = c->lh[L]; }
+        pa.nlev = c->nlev; pa.S = c->S;
+        klt_pyramid_kernel<<<dim3((c->lw[1] + 15) / 16, (c->lh[1] + 15) / 16, 2 * c->S), 256, 0, c->side>>>(pa);
+        if ((fe = cudaGetLastError()) != cudaSuccess) return fe;
+        return cudaEventRecord(c->ev_pyr, c->side);
+    };
+    if (e == cudaSuccess) e = launch_corners(c, prev, ppitch, c->corners, c->counts, st, fork_pyramid);
+    if (e == cudaSuccess && c->nlev > 1) e = cudaStreamWaitEvent(st, c->ev_pyr, 0);
+    if (e == cudaSuccess)
+        e = launch_track(c, prev, ppitch, next, npitch, c->corners, c->counts, c->tracked, c->status, st, true);
     if (e == cudaSuccess) {
         CompactArgs ca;
         ca.corners = c->corners; ca.counts = c->counts; ca.tracked = c->tracked; ca.status = c->status;
@@ -319,6 +349,9 @@ void dmsgm_klt_destroy(dmsgm_klt_ctx* c) {
         if (q) cudaFree(q);
     for (int L = 0; L < kMaxLevels; ++L)
         if (c->pyr[L]) cudaFree(c->pyr[L]);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_pyr) cudaEventDestroy(c->ev_pyr);
     delete c;
 }
 

@@ -337,7 +337,9 @@ __global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArg
     unsigned long long* batch = reinterpret_cast<unsigned long long*>(sm);      // [kBatch]
     unsigned* hist = reinterpret_cast<unsigned*>(batch + kBatch);               // [256]
     int* kept = reinterpret_cast<int*>(hist + 256);                             // [kMaxCorners][2]
-    uint16_t* grid_s = reinterpret_cast<uint16_t*>(kept + 2 * kMaxCorners);
+    uint32_t* pxy = reinterpret_cast<uint32_t*>(kept + 2 * kMaxCorners);        // [kBatch] x | y << 16
+    uint32_t* pcell = pxy + kBatch;                                              // [kBatch] cx | cy << 16
+    uint16_t* grid_s = reinterpret_cast<uint16_t*>(pcell + kBatch);
     __shared__ unsigned long long s_prefix, s_mask;
     __shared__ unsigned s_rem, s_total, s_m;
     __shared__ int s_nkept, s_done;
@@ -417,15 +419,24 @@ __global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArg
                 }
                 __syncthreads();
             }
+        // ---- decode the batch in parallel: pixel and greedy cell of every key ----
+        for (int j = tid; j < m; j += kSelThreads) {
+            const unsigned idx = 0xFFFFFFFFu - (unsigned)batch[j];
+            const int y = (int)(idx / (unsigned)a.W), x = (int)(idx - (unsigned)y * (unsigned)a.W);
+            pxy[j] = (uint32_t)x | ((uint32_t)y << 16);
+            pcell[j] = (uint32_t)(x / a.cell) | ((uint32_t)(y / a.cell) << 16);
+        }
+        __syncthreads();
         // ---- greedy selection by warp 0: a cell holds at most one kept corner ----
         if (tid < 32) {
             const int lane = tid;
             int nk = s_nkept;
             const int dx = lane % 5 - 2, dy = lane / 5 - 2;
+            uint32_t nxy = m > 0 ? pxy[0] : 0u, ncell = m > 0 ? pcell[0] : 0u;     // next key, loaded ahead
             for (int j = 0; j < m && nk < a.max_corners; ++j) {
-                const unsigned idx = 0xFFFFFFFFu - (unsigned)batch[j];
-                const int y = (int)(idx / (unsigned)a.W), x = (int)(idx - (unsigned)y * (unsigned)a.W);
-                const int cx = x / a.cell, cy = y / a.cell;
+                const int x = (int)(nxy & 0xFFFFu), y = (int)(nxy >> 16);
+                const int cx = (int)(ncell & 0xFFFFu), cy = (int)(ncell >> 16);
+                if (j + 1 < m) { nxy = pxy[j + 1]; ncell = pcell[j + 1]; }
                 bool conflict = false;
                 if (lane < 25) {
                     const int gx = cx + dx, gy = cy + dy;
