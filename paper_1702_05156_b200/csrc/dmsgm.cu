@@ -67,6 +67,7 @@ struct dmsgm_ctx {
     int staged_occ;    // register-capped occupancy variant (3 or 4 CTAs/SM)
     unsigned* item_ctr;   // [kCounterSlots] dynamic item counters of the staged kernel (0 between launches)
     int pdl;           // programmatic dependent launch of consecutive steps (DMSGM_PDL=0 disables)
+    int gen_bpt;       // register-path kernel at N = 4: forced blocks per thread (0 = automatic)
     CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (4-D: 96-B chunks of 4 records)
     // row band; whole frame: row0 = 0, rows = Hb, halo = 0, band = 0
     int band, row0, rows, halo;
@@ -285,7 +286,11 @@ int bpt_of(const dmsgm_ctx* c) {
     switch (c->N) {
         case 1: return 4;
         case 2: return 2;
-        case 4: return (c->Wb % 2 == 0) ? 2 : 1;
+        case 4:
+            // DMSGM_GENERIC_BPT = 1 / 2 / 4 at dmsgm_create: blocks per thread of the register-path
+            // kernel at N = 4 (32- / 64- / 128-bit pixel-row loads; the SURVEY §8(d) ablation)
+            if (c->gen_bpt && c->Wb % c->gen_bpt == 0) return c->gen_bpt;
+            return (c->Wb % 2 == 0) ? 2 : 1;
         default: return 1;
     }
 }
@@ -474,6 +479,7 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
         case 2 * 16 + 2: launch_kernel<2, 2>(a, grid, block, stream); break;
         case 4 * 16 + 2: launch_kernel<4, 2>(a, grid, block, stream); break;
         case 4 * 16 + 1: launch_kernel<4, 1>(a, grid, block, stream); break;
+        case 4 * 16 + 4: launch_kernel<4, 4>(a, grid, block, stream); break;
         case 8 * 16 + 1: launch_kernel<8, 1>(a, grid, block, stream); break;
         case 16 * 16 + 1: launch_kernel<16, 1>(a, grid, block, stream); break;
         default: return cudaErrorInvalidValue;
@@ -580,6 +586,9 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
     {
         const char* kenv = getenv("DMSGM_KERNEL");           // "generic" forces the register-path kernel
         const bool want = !(kenv && strcmp(kenv, "generic") == 0);
+        const char* benv = getenv("DMSGM_GENERIC_BPT");
+        c->gen_bpt = benv ? atoi(benv) : 0;
+        if (c->gen_bpt != 1 && c->gen_bpt != 2 && c->gen_bpt != 4) c->gen_bpt = 0;
         c->staged = 0;
         if (want && block != 16) {   // N = 16: a 512-byte frame row exceeds the TMA box limit
             const char* oenv = getenv("DMSGM_STAGED_OCC");   // 3 or 4 resident CTAs per SM (register cap)

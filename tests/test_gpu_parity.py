@@ -20,12 +20,17 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 IDENT = np.eye(3).reshape(9)
 
 
-@pytest.fixture(params=["default", "generic"])
+@pytest.fixture(params=["default", "generic", "generic_bpt1", "generic_bpt4"])
 def kernel_path(request, monkeypatch):
     """default: the persistent shared-memory-staged kernel where it applies (N = 4 with
-    even Wb, N = 8); generic: force the register-path kernel (DMSGM_KERNEL=generic)."""
-    if request.param == "generic":
+    even Wb, N = 8); generic: force the register-path kernel (DMSGM_KERNEL=generic);
+    generic_bpt1 / _bpt4: that kernel with 1 / 4 blocks per thread at N = 4 (32- / 128-bit
+    pixel-row loads, the SURVEY §8(d) ablation variants; other N unchanged)."""
+    monkeypatch.delenv("DMSGM_GENERIC_BPT", raising=False)
+    if request.param.startswith("generic"):
         monkeypatch.setenv("DMSGM_KERNEL", "generic")
+        if request.param != "generic":
+            monkeypatch.setenv("DMSGM_GENERIC_BPT", request.param[-1])
     else:
         monkeypatch.delenv("DMSGM_KERNEL", raising=False)
     return request.param
