@@ -366,9 +366,20 @@ __global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArg
             if (tid < 256) hist[tid] = 0;
             __syncthreads();
             const unsigned long long pre = s_prefix, msk = s_mask;
-            for (int i = tid; i < n; i += kSelThreads) {
-                const unsigned long long k = cand[i];
-                if (k < upper && (k & msk) == pre && qualifies(k, thr)) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+            // 8 keys per thread in flight (one load at a time left the pass latency-bound)
+            for (int i0 = tid; i0 < n; i0 += 8 * kSelThreads) {
+                unsigned long long kk[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * kSelThreads;
+                    kk[u] = i < n ? cand[i] : ~0ull;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const unsigned long long k = kk[u];
+                    if (i0 + u * kSelThreads < n && k < upper && (k & msk) == pre && qualifies(k, thr))
+                        atomicAdd(&hist[(k >> shift) & 255u], 1u);
+                }
             }
             __syncthreads();
             if (tid == 0) {
@@ -396,9 +407,24 @@ __global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArg
         // ---- gather the batch: qualifying keys in [cut, upper) ----
         if (tid == 0) s_m = 0;
         __syncthreads();
-        for (int i = tid; i < n; i += kSelThreads) {
-            const unsigned long long k = cand[i];
-            if (k < upper && k >= cut && qualifies(k, thr)) batch[atomicAdd(&s_m, 1u)] = k;
+        for (int i0 = tid & ~31; i0 < n; i0 += 4 * kSelThreads) {       // warp-aggregated append
+            unsigned long long kk[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kSelThreads + (tid & 31);
+                kk[u] = i < n ? cand[i] : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kSelThreads + (tid & 31);
+                const unsigned long long k = kk[u];
+                const bool in = i < n && k < upper && k >= cut && qualifies(k, thr);
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                unsigned b0 = 0;
+                if ((tid & 31) == 0 && bal) b0 = atomicAdd(&s_m, (unsigned)__popc(bal));
+                b0 = __shfl_sync(0xffffffffu, b0, 0);
+                if (in) batch[b0 + __popc(bal & ((1u << (tid & 31)) - 1u))] = k;
+            }
         }
         __syncthreads();
         const int m = (int)s_m;
@@ -427,39 +453,57 @@ __global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArg
             pcell[j] = (uint32_t)(x / a.cell) | ((uint32_t)(y / a.cell) << 16);
         }
         __syncthreads();
-        // ---- greedy selection by warp 0: a cell holds at most one kept corner ----
+        // ---- greedy selection by warp 0, 32 keys at a time (a cell holds at most one kept
+        //      corner; cells of side ceil(d / sqrt 2), so a conflict lies within +-2 cells):
+        //      (1) each lane tests its key against the corners kept so far (grid);
+        //      (2) each lane collects which EARLIER surviving keys of the chunk lie within d;
+        //      (3) a 32-step scan in rank order keeps a survivor iff none of its earlier
+        //          conflicting survivors was kept -- exactly the sequential greedy's decisions;
+        //      (4) the kept ones are appended in rank order (up to max_corners). ----
         if (tid < 32) {
             const int lane = tid;
             int nk = s_nkept;
-            const int dx = lane % 5 - 2, dy = lane / 5 - 2;
-            uint32_t nxy = m > 0 ? pxy[0] : 0u, ncell = m > 0 ? pcell[0] : 0u;     // next key, loaded ahead
-            for (int j = 0; j < m && nk < a.max_corners; ++j) {
-                const int x = (int)(nxy & 0xFFFFu), y = (int)(nxy >> 16);
-                const int cx = (int)(ncell & 0xFFFFu), cy = (int)(ncell >> 16);
-                if (j + 1 < m) { nxy = pxy[j + 1]; ncell = pcell[j + 1]; }
+            for (int base = 0; base < m && nk < a.max_corners; base += 32) {
+                const int j = base + lane;
+                const bool valid = j < m;
+                const uint32_t xy = valid ? pxy[j] : 0u, ce = valid ? pcell[j] : 0u;
+                const int x = (int)(xy & 0xFFFFu), y = (int)(xy >> 16);
+                const int cx = (int)(ce & 0xFFFFu), cy = (int)(ce >> 16);
                 bool conflict = false;
-                if (lane < 25) {
-                    const int gx = cx + dx, gy = cy + dy;
-                    if (gx >= 0 && gx < a.gw && gy >= 0 && gy < a.gh) {
-                        const int e = *(volatile uint16_t*)(grid + gy * a.gw + gx);
-                        if (e) {
-                            const int kx = kept[2 * (e - 1)], ky = kept[2 * (e - 1) + 1];
-                            const int ddx = x - kx, ddy = y - ky;
-                            conflict = (double)(ddx * ddx + ddy * ddy) < a.min_dist2;
+                if (valid) {
+                    for (int gy = max(cy - 2, 0); gy <= min(cy + 2, a.gh - 1) && !conflict; ++gy)
+                        for (int gx = max(cx - 2, 0); gx <= min(cx + 2, a.gw - 1); ++gx) {
+                            const int e = grid[gy * a.gw + gx];
+                            if (e) {
+                                const int ddx = x - kept[2 * (e - 1)], ddy = y - kept[2 * (e - 1) + 1];
+                                if ((double)(ddx * ddx + ddy * ddy) < a.min_dist2) { conflict = true; break; }
+                            }
                         }
-                    }
                 }
-                if (!__any_sync(0xffffffffu, conflict)) {
-                    if (lane == 0) {
-                        kept[2 * nk] = x;
-                        kept[2 * nk + 1] = y;
-                        *(volatile uint16_t*)(grid + cy * a.gw + cx) = (uint16_t)(nk + 1);
-                        a.corners_out[((long long)s * a.max_corners + nk) * 2] = x;
-                        a.corners_out[((long long)s * a.max_corners + nk) * 2 + 1] = y;
-                    }
-                    ++nk;
-                    __syncwarp();
+                const unsigned surv = __ballot_sync(0xffffffffu, valid && !conflict);
+                unsigned earlier = 0;                   // earlier survivors of the chunk within d
+                for (int k = 0; k < 32; ++k) {
+                    const int xk = __shfl_sync(0xffffffffu, x, k), yk = __shfl_sync(0xffffffffu, y, k);
+                    const int ddx = x - xk, ddy = y - yk;
+                    if (k < lane && ((surv >> k) & 1u) && (double)(ddx * ddx + ddy * ddy) < a.min_dist2)
+                        earlier |= 1u << k;
                 }
+                unsigned keep = 0;
+                int room = a.max_corners - nk;
+                for (int k = 0; k < 32 && room > 0; ++k) {
+                    const unsigned ek = __shfl_sync(0xffffffffu, earlier, k);
+                    if (((surv >> k) & 1u) && !(ek & keep)) { keep |= 1u << k; --room; }
+                }
+                if ((keep >> lane) & 1u) {
+                    const int idx = nk + __popc(keep & ((1u << lane) - 1u));
+                    kept[2 * idx] = x;
+                    kept[2 * idx + 1] = y;
+                    grid[cy * a.gw + cx] = (uint16_t)(idx + 1);
+                    a.corners_out[((long long)s * a.max_corners + idx) * 2] = x;
+                    a.corners_out[((long long)s * a.max_corners + idx) * 2 + 1] = y;
+                }
+                nk += __popc(keep);
+                __syncwarp();
             }
             if (lane == 0) {
                 s_nkept = nk;
