@@ -616,10 +616,13 @@ __device__ __forceinline__ float pix_clamped(const uint8_t* img, int pitch, int 
 constexpr int kLkWarps = 8;
 constexpr int kLkMaxWin = 32;
 
+#ifndef DMSGM_LK_MINB
+#define DMSGM_LK_MINB 3
+#endif
 constexpr int kLkMargin = 4;     // next-image region: the window +- this many pixels of flow per level
 
 template <int NS>   // samples per lane: ceil(win^2 / 32)
-__global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? 3 : 1) klt_lk_kernel(const LkArgs a) {
+__global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) klt_lk_kernel(const LkArgs a) {
     constexpr int MW = NS <= 8 ? 16 : (NS <= 13 ? 20 : kLkMaxWin);   // largest window of this variant
     constexpr bool STAGE = NS <= 13;       // (win > 20: the regions would exceed 48 KB; global reads)
     constexpr int MR = STAGE ? MW + 1 + 2 * kLkMargin : 1;             // next-region side
@@ -649,7 +652,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? 3 : 1) klt_lk_kernel
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         const int q = lane + 32 * k, jj = q / win;
-        roff[k] = jj * rs + (q - jj * win);
+        roff[k] = q < nsamp ? jj * rs + (q - jj * win) : 0;
     }
     float gx = 0.0f, gy = 0.0f;
     bool ok = true;
@@ -668,18 +671,24 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? 3 : 1) klt_lk_kernel
             const float fx = __fsub_rn(ux, xf), fy = __fsub_rn(uy, yf);
             const float gxw = __fsub_rn(1.0f, fx), gyw = __fsub_rn(1.0f, fy);
             const int X0 = (int)xf, Y0 = (int)yf;
-            // patch[(jj + 1) * pw + (ii + 1)] = bil(prev, sample (ii, jj)), ii, jj in [-1, win]
+            // patch[(jj + 1) * pw + (ii + 1)] = bil(prev, sample (ii, jj)), ii, jj in [-1, win]:
+            // row by row, lane = column (pw <= 34 columns: lanes 0-31, then a second pass)
             __syncwarp();
-#pragma unroll 4
-            for (int q = lane; q < pw * pw; q += 32) {
-                const int jj = q / pw - 1, ii = q - (jj + 1) * pw - 1;
-                const int x = X0 + ii, y = Y0 + jj;
-                const float p00 = pix_clamped(pp, P.pitch, P.w, P.h, x, y), p10 = pix_clamped(pp, P.pitch, P.w, P.h, x + 1, y);
-                const float p01 = pix_clamped(pp, P.pitch, P.w, P.h, x, y + 1),
-                            p11 = pix_clamped(pp, P.pitch, P.w, P.h, x + 1, y + 1);
-                const float top = __fadd_rn(__fmul_rn(p00, gxw), __fmul_rn(p10, fx));
-                const float bot = __fadd_rn(__fmul_rn(p01, gxw), __fmul_rn(p11, fx));
-                patch[q] = __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy));
+            for (int c0 = 0; c0 < pw; c0 += 32) {
+                const int ci = c0 + lane;                   // patch column
+                if (ci < pw) {
+                    const int x = X0 + ci - 1;
+                    const int xa = clampi(x, 0, P.w - 1), xb = clampi(x + 1, 0, P.w - 1);
+                    // row y's horizontal blend is row y+1's top: computed once per image row
+                    const uint8_t* r0 = pp + (long long)clampi(Y0 - 1, 0, P.h - 1) * P.pitch;
+                    float top = __fadd_rn(__fmul_rn((float)__ldg(r0 + xa), gxw), __fmul_rn((float)__ldg(r0 + xb), fx));
+                    for (int rj = 0; rj < pw; ++rj) {
+                        const uint8_t* rb = pp + (long long)clampi(Y0 + rj, 0, P.h - 1) * P.pitch;
+                        const float bot = __fadd_rn(__fmul_rn((float)__ldg(rb + xa), gxw), __fmul_rn((float)__ldg(rb + xb), fx));
+                        patch[rj * pw + ci] = __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy));
+                        top = bot;
+                    }
+                }
             }
             __syncwarp();
         }
@@ -693,10 +702,16 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? 3 : 1) klt_lk_kernel
             RX0 = STAGE ? (int)floorf(ux) - kLkMargin : INT_MIN / 2;      // INT_MIN / 2: never inside
             RY0 = (int)floorf(uy) - kLkMargin;
             __syncwarp();
-#pragma unroll 4
-            for (int q = lane; STAGE && q < rs * rs; q += 32) {
-                const int jj = q / rs, ii = q - jj * rs;
-                region[q] = pix_clamped(qp, Q.pitch, Q.w, Q.h, RX0 + ii, RY0 + jj);
+            if (STAGE) {
+                for (int c0 = 0; c0 < rs; c0 += 32) {
+                    const int ci = c0 + lane;
+                    if (ci < rs) {
+                        const int xa = clampi(RX0 + ci, 0, Q.w - 1);
+                        for (int rj = 0; rj < rs; ++rj)
+                            region[rj * rs + ci] =
+                                (float)__ldg(qp + (long long)clampi(RY0 + rj, 0, Q.h - 1) * Q.pitch + xa);
+                    }
+                }
             }
             __syncwarp();
         }
@@ -743,19 +758,19 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? 3 : 1) klt_lk_kernel
             const int X0 = (int)xf, Y0 = (int)yf;
             const int dxr = X0 - RX0, dyr = Y0 - RY0;
             if ((unsigned)dxr <= 2u * kLkMargin && (unsigned)dyr <= 2u * kLkMargin) {
-                // the window (and its +1 neighbours) inside the staged region
+                // the window (and its +1 neighbours) inside the staged region; branch-free: a
+                // lane's padding samples (q >= win^2) read offset 0 and have I = Ix = Iy = 0, so
+                // they add exactly +0 to both sums
                 const float* base = region + dyr * rs + dxr;
 #pragma unroll
                 for (int k = 0; k < NS; ++k) {
-                    if (lane + 32 * k < nsamp) {
-                        const float* r0 = base + roff[k];
-                        const float p00 = r0[0], p10 = r0[1], p01 = r0[rs], p11 = r0[rs + 1];
-                        const float top = __fadd_rn(__fmul_rn(p00, gxw), __fmul_rn(p10, fx));
-                        const float bot = __fadd_rn(__fmul_rn(p01, gxw), __fmul_rn(p11, fx));
-                        const float e = __fsub_rn(I[k], __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy)));
-                        bx = __fadd_rn(bx, __fmul_rn(e, Ix[k]));
-                        by = __fadd_rn(by, __fmul_rn(e, Iy[k]));
-                    }
+                    const float* r0 = base + roff[k];
+                    const float p00 = r0[0], p10 = r0[1], p01 = r0[rs], p11 = r0[rs + 1];
+                    const float top = __fadd_rn(__fmul_rn(p00, gxw), __fmul_rn(p10, fx));
+                    const float bot = __fadd_rn(__fmul_rn(p01, gxw), __fmul_rn(p11, fx));
+                    const float e = __fsub_rn(I[k], __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy)));
+                    bx = __fadd_rn(bx, __fmul_rn(e, Ix[k]));
+                    by = __fadd_rn(by, __fmul_rn(e, Iy[k]));
                 }
             } else {
 #pragma unroll
