@@ -151,19 +151,10 @@ struct ScoreLane {
     float sl, s0[4], sr;      // a score row: left neighbour column, own 4, right neighbour column
 };
 
-// Non-negative integer v < 2^52 as a double without the conversion pipe: the bits of 2^52 + v
-// minus 2^52 (exact).
-__device__ __forceinline__ double klt_u52_to_double(unsigned long long v) {
-    return __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ull | v)), 4503599627370496.0);
-}
 __device__ __forceinline__ float klt_lambda_min(int a, int b, int c) {
-    // the discriminant as an exact 64-bit integer (< 2^51), a + c >= 0 (< 2^24): both exact
-    // doubles by the 2^52 trick, the same values as the casts (identical result)
-    const long long t = (long long)(a - c), bb = (long long)b;
-    const unsigned long long D = (unsigned long long)(t * t + 4 * bb * bb);
-    const double d = klt_u52_to_double(D);
-    const double ac = klt_u52_to_double((unsigned long long)(a + c));
-    return __double2float_rn(__dmul_rn(__dsub_rn(ac, __dsqrt_rn(d)), 0.5));
+    const double t = (double)(a - c), tb = (double)b;
+    const double d = __fma_rn(t, t, __dmul_rn(4.0 * tb, tb));        // exact: < 2^51
+    return __double2float_rn(__dmul_rn(__dsub_rn((double)(a + c), __dsqrt_rn(d)), 0.5));
 }
 
 __global__ void __launch_bounds__(32 * kScoreWarps) klt_score_stream_kernel(const ScoreArgs a) {
