@@ -439,21 +439,42 @@ def run_dmsgm(args, rank, world, local):
             ctx.step_host(hf, hH[i % RING], hm, stream)
         if world > 1:
             dist.barrier()
-        hm2 = [hm, torch.empty_like(hm).pin_memory()]
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        for i in range(e2e_steps):
-            # the step's inputs are already in pinned host memory (written by the "producer"
-            # outside the timed region); every step copies its frames and homographies H2D,
-            # computes, and copies its masks D2H.  dmsgm_step_host_async lets step i+1's
-            # uploads overlap step i's downloads; one sync ends the timed region.
-            ctx.step_host_async(ring_host[i % len(ring_host)], hH[i % RING], hm2[i % 2], stream)
-        torch.cuda.synchronize(dev)
-        e2e_s = max_over_ranks(time.perf_counter() - t0, red_dev)
+        def e2e_run(hmasks):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            for i in range(e2e_steps):
+                # the step's inputs are already in pinned host memory (written by the "producer"
+                # outside the timed region); every step copies its frames and homographies H2D,
+                # computes, and copies its masks D2H.  dmsgm_step_host_async lets step i+1's
+                # uploads overlap step i's downloads; one sync ends the timed region.
+                ctx.step_host_async(ring_host[i % len(ring_host)], hH[i % RING], hmasks[i % 2], stream)
+            torch.cuda.synchronize(dev)
+            return max_over_ranks(time.perf_counter() - t0, red_dev)
+
+        e2e_s = e2e_run([hm, torch.empty_like(hm).pin_memory()])
         e2e = {"value": total_streams * e2e_steps / e2e_s, "unit": "frames/s",
                "h2d_bytes_per_step": S * H * W + S * 9 * 8, "d2h_bytes_per_step": S * H * W,
-               "steps": e2e_steps,
+               "steps": e2e_steps, "mask_format": "bytes (0 / 255 per pixel)",
                "api": "dmsgm_step_host_async (pinned host buffers; all copies inside the timed region)"}
+        # the same API with DMSGM_MASK_BITS: identical decisions, one bit per pixel, an eighth
+        # of the D2H bytes (the link is the bound: DESIGN.md §6.3).  Reported beside; `value`
+        # stays the byte-mask figure.
+        try:
+            ctx.set_mask_format(dm.DMSGM_MASK_BITS)
+        except dm.DmsgmError:
+            pass
+        else:
+            mw = (W + 7) // 8
+            hb = [torch.empty((S, H, mw), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            for i in range(2):
+                ctx.step_host(ring_host[i % len(ring_host)], hH[i % RING], hb[0], stream)
+            eb_s = e2e_run(hb)
+            e2e["bit_masks"] = {"value": total_streams * e2e_steps / eb_s, "unit": "frames/s",
+                                "h2d_bytes_per_step": S * H * W + S * 9 * 8, "d2h_bytes_per_step": S * H * mw,
+                                "steps": e2e_steps, "api": "dmsgm_step_host_async + dmsgm_set_mask_format(BITS)"}
+            ctx.set_mask_format(dm.DMSGM_MASK_BYTES)
 
     # ---- CPU oracle baseline (rank 0 at N=1 only) ----
     cpu = None

@@ -196,6 +196,21 @@ int dmsgm_prefilter(int width, int height, int count, const uint8_t* in, size_t 
  * Synchronises the device. */
 int dmsgm_set_motion(dmsgm_ctx* ctx, int mode);
 
+/* ------------------------------------------------------------------------------------
+ * Mask format.  DMSGM_MASK_BYTES (default): one byte per pixel, 0 or 255 (App. E
+ * writes 255 for foreground).  DMSGM_MASK_BITS: one bit per pixel, 1 = foreground, row y
+ * of stream s at masks + s*height*mask_pitch + y*mask_pitch, pixel x in byte x/8, bit x%8
+ * (least significant first: numpy.packbits(mask > 0, bitorder="little")); mask_pitch >=
+ * ceil(width / 8), a multiple of 16.  The same decisions, an eighth of the bytes -- what
+ * dmsgm_step_host(_async) then copies back over PCIe.  Requires the staged kernel (block 4
+ * or 8, width / block a multiple of 32) in whole-frame mode; DMSGM_EINVAL otherwise.
+ * ------------------------------------------------------------------------------------ */
+#define DMSGM_MASK_BYTES 0
+#define DMSGM_MASK_BITS  1
+
+/* Select the mask format of every later step call.  Synchronises the device. */
+int dmsgm_set_mask_format(dmsgm_ctx* ctx, int format);
+
 /* Stand-alone frame warp of `count` frames: in / out u8 [count][height][pitch] (device,
  * width % 4 == 0, 4-byte aligned pitches and bases), homographies f64 [count][9]
  * (device, frame t -> frame t-1 as for the step).  Enqueued on cuda_stream. */

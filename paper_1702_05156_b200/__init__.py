@@ -9,7 +9,7 @@ a fresh checkout; touching any API name loads libdmsgm.so and raises ImportError
 is missing (there is no CPU fallback).
 """
 _API = ("Dmsgm", "DmsgmError", "Params", "dmsgm_params", "dmsgm_info", "dmsgm_buffers", "band_halo_needed", "prefilter", "warp_frames",
-        "DMSGM_MC_MODELS", "DMSGM_MC_FRAME",
+        "DMSGM_MC_MODELS", "DMSGM_MC_FRAME", "DMSGM_MASK_BYTES", "DMSGM_MASK_BITS",
         "DMSGM_IPC_BYTES", "lib", "load_library", "version",
         "EXPORTS", "DMSGM_OK", "DMSGM_EINVAL", "DMSGM_ENOMEM", "DMSGM_ECUDA", "DMSGM_ESTATE")
 

@@ -68,6 +68,7 @@ struct dmsgm_ctx {
     unsigned* item_ctr;   // [kCounterSlots] dynamic item counters of the staged kernel (0 between launches)
     int pdl;           // programmatic dependent launch of consecutive steps (DMSGM_PDL=0 disables)
     int gen_bpt;       // register-path kernel at N = 4: forced blocks per thread (0 = automatic)
+    int mask_bits;     // DMSGM_MASK_BITS: 1 bit per pixel (staged kernel, whole frame)
     CUtensorMap state_map[2];   // TMA descriptors of the two state buffers (4-D: 96-B chunks of 4 records)
     // row band; whole frame: row0 = 0, rows = Hb, halo = 0, band = 0
     int band, row0, rows, halo;
@@ -138,7 +139,7 @@ bool encode_state_map(const dmsgm_ctx* c, float* base, int xc, int wrows, CUtens
 }  // namespace
 
 // Persistent TMA-staged kernel (N = 4 / 8): grid = resident CTAs (computed once per context).
-template <int N, int BPT, int MINB, bool RULES, bool BAND = false>
+template <int N, int BPT, int MINB, bool RULES, bool BAND = false, bool MBITS = false>
 cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames, size_t fpitch, int s0,
                           int count, int parity, int slot, cudaStream_t stream, bool early_frames) {
     StagedArgs sa;
@@ -164,7 +165,7 @@ cudaError_t launch_staged(dmsgm_ctx* c, const StepArgs& a, const uint8_t* frames
     attr[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, dmsgm_step_staged<N, BPT, MINB, RULES, BAND>, a, sa, fmap,
+    return cudaLaunchKernelEx(&cfg, dmsgm_step_staged<N, BPT, MINB, RULES, BAND, MBITS>, a, sa, fmap,
                               c->state_map[parity]);
 }
 
@@ -175,6 +176,14 @@ cudaError_t setup_staged(dmsgm_ctx* c) {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT>::SMEM_BYTES);
+    if constexpr (MINB == 3 && (N == 4 || N == 8)) {   // the bit-mask variants (DMSGM_MASK_BITS)
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT>::SMEM_BYTES);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, true, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Staged<N, BPT>::SMEM_BYTES);
+    }
     if constexpr (MINB == 3) {   // the band-mode variants (default configuration only)
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(dmsgm_step_staged<N, BPT, MINB, false, true>,
@@ -464,7 +473,13 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
                                                    early_frames)                                               \
                  : launch_staged<NN, BB, OO, false>(c, a, frames, fpitch, s0, count, parity, slot, stream,      \
                                                     early_frames)
+#define DMSGM_STAGED_BITS(NN, BB)                                                                          \
+    return rules ? launch_staged<NN, BB, 3, true, false, true>(c, a, frames, fpitch, s0, count, parity, slot,  \
+                                                              stream, early_frames)                          \
+                 : launch_staged<NN, BB, 3, false, false, true>(c, a, frames, fpitch, s0, count, parity, slot, \
+                                                               stream, early_frames)
 #define DMSGM_STAGED_OCC(NN, BB)                      \
+    if (c->mask_bits) { DMSGM_STAGED_BITS(NN, BB); }  \
     if (c->staged_occ == 3) { DMSGM_STAGED(NN, BB, 3); } \
     DMSGM_STAGED(NN, BB, 4)
         if (c->N == 1) { DMSGM_STAGED(1, 2, 3); }
@@ -472,6 +487,7 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
         if (c->N == 4) { DMSGM_STAGED_OCC(4, 2); }
         if (c->N == 8) { DMSGM_STAGED_OCC(8, 1); }
 #undef DMSGM_STAGED_OCC
+#undef DMSGM_STAGED_BITS
 #undef DMSGM_STAGED
     }
     switch (c->N * 16 + bpt) {
@@ -494,7 +510,9 @@ int check_images(dmsgm_ctx* c, const void* frames, size_t fpitch, const void* H,
         return fail(c, DMSGM_EINVAL, "frames and masks must be 16-byte aligned");
     if ((uintptr_t)H & 7) return fail(c, DMSGM_EINVAL, "homographies must be 8-byte aligned");
     if (fpitch < (size_t)c->W || (fpitch & 15)) return fail(c, DMSGM_EINVAL, "frame_pitch must be >= width and a multiple of 16");
-    if (mpitch < (size_t)c->W || (mpitch & 15)) return fail(c, DMSGM_EINVAL, "mask_pitch must be >= width and a multiple of 16");
+    const size_t mrow = c->mask_bits ? ((size_t)c->W + 7) / 8 : (size_t)c->W;     // bytes of one mask row
+    if (mpitch < mrow || (mpitch & 15))
+        return fail(c, DMSGM_EINVAL, "mask_pitch must be >= %zu (the mask row) and a multiple of 16", mrow);
     if ((double)fpitch * c->Hp > 2147483647.0 || (double)mpitch * c->Hp > 2147483647.0)
         return fail(c, DMSGM_EINVAL, "one image (pitch x height) must be < 2 GiB");
     return DMSGM_OK;
@@ -707,13 +725,15 @@ int step_host_impl(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double*
                    void* cuda_stream, bool async) {
     if (!c) return DMSGM_EINVAL;
     if (!hf || !hH || !hm) return fail(c, DMSGM_EINVAL, "null host pointer");
-    if (fpitch < (size_t)c->W || mpitch < (size_t)c->W)
-        return fail(c, DMSGM_EINVAL, "pitches must be >= width");
+    if (fpitch < (size_t)c->W) return fail(c, DMSGM_EINVAL, "frame_pitch must be >= width");
     DeviceGuard g(c->device);
     if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
     cudaError_t e;
     const size_t dpitch = ((size_t)c->W + 15) & ~(size_t)15;
     const size_t fimg = (size_t)c->Hp * dpitch;
+    const size_t mrow = c->mask_bits ? ((size_t)c->W + 7) / 8 : (size_t)c->W;   // bytes per mask row
+    const size_t dmpitch = (mrow + 15) & ~(size_t)15, mimg = (size_t)c->Hp * dmpitch;
+    if (mpitch < mrow) return fail(c, DMSGM_EINVAL, "mask_pitch must be >= %zu (the mask row)", mrow);
     int rc = check_status(c);
     if (rc) return rc;
     bool first = false;
@@ -780,7 +800,7 @@ int step_host_impl(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double*
         const int cnt = (c->S - s0) < per ? (c->S - s0) : per;
         cudaStream_t st = c->pipe[k % kPipeStreams];
         uint8_t* df = c->st_frames + (size_t)s0 * fimg;
-        uint8_t* dm = c->st_masks + (size_t)s0 * fimg;
+        uint8_t* dm = c->st_masks + (size_t)s0 * mimg;
         if ((e = cudaMemcpy2DAsync(df, dpitch, hf + (size_t)s0 * c->Hp * fpitch, fpitch, c->W, (size_t)cnt * c->Hp,
                                    cudaMemcpyHostToDevice, st)) != cudaSuccess)
             return cuda_fail(c, e, "H2D frames");
@@ -788,10 +808,10 @@ int step_host_impl(dmsgm_ctx* c, const uint8_t* hf, size_t fpitch, const double*
                                  cudaMemcpyHostToDevice, st)) != cudaSuccess)
             return cuda_fail(c, e, "H2D homographies");
         // chunks run concurrently on the pipe streams: each its own item-counter slot
-        if ((e = launch_step(c, df, dpitch, c->st_H + (size_t)s0 * 9, dm, dpitch, s0, cnt, parity, st,
+        if ((e = launch_step(c, df, dpitch, c->st_H + (size_t)s0 * 9, dm, dmpitch, s0, cnt, parity, st,
                              1 + k % (kCounterSlots - 1))) != cudaSuccess)
             return cuda_fail(c, e, "dmsgm_step_host launch");
-        if ((e = cudaMemcpy2DAsync(hm + (size_t)s0 * c->Hp * mpitch, mpitch, dm, dpitch, c->W, (size_t)cnt * c->Hp,
+        if ((e = cudaMemcpy2DAsync(hm + (size_t)s0 * c->Hp * mpitch, mpitch, dm, dmpitch, mrow, (size_t)cnt * c->Hp,
                                    cudaMemcpyDeviceToHost, st)) != cudaSuccess)
             return cuda_fail(c, e, "D2H masks");
     }
@@ -973,6 +993,22 @@ int dmsgm_warp_frames(int width, int height, int count, const uint8_t* in, size_
     return e == cudaSuccess ? DMSGM_OK : DMSGM_ECUDA;
 }
 
+int dmsgm_set_mask_format(dmsgm_ctx* c, int format) {
+    if (!c) return DMSGM_EINVAL;
+    if (format != DMSGM_MASK_BYTES && format != DMSGM_MASK_BITS)
+        return fail(c, DMSGM_EINVAL, "format must be DMSGM_MASK_BYTES or DMSGM_MASK_BITS");
+    if (format == DMSGM_MASK_BITS &&
+        (!c->staged || c->staged_occ != 3 || (c->N != 4 && c->N != 8) || c->Wb % kCtaX != 0 || c->band))
+        return fail(c, DMSGM_EINVAL, "bit masks need the staged kernel (block 4 or 8, width / block a multiple of "
+                                     "32) in whole-frame mode");
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "dmsgm_set_mask_format sync");
+    destroy_graphs(c);
+    c->mask_bits = format == DMSGM_MASK_BITS ? 1 : 0;
+    return DMSGM_OK;
+}
+
 int dmsgm_set_motion(dmsgm_ctx* c, int mode) {
     if (!c) return DMSGM_EINVAL;
     if (mode != DMSGM_MC_MODELS && mode != DMSGM_MC_FRAME)
@@ -1040,6 +1076,8 @@ int dmsgm_set_band(dmsgm_ctx* c, int row0, int rows, int halo) {
     if (halo < 0 || halo > rows) return fail(c, DMSGM_EINVAL, "halo must be in [0, rows]");
     if ((c->pf_buf || c->wf_buf) && !(row0 == 0 && rows == c->Hb && halo == 0))
         return fail(c, DMSGM_ESTATE, "preprocessing / frame warping is not supported in row-band mode");
+    if (c->mask_bits && !(row0 == 0 && rows == c->Hb && halo == 0))
+        return fail(c, DMSGM_ESTATE, "bit masks are not supported in row-band mode");
     DeviceGuard g(c->device);
     if (!g.ok) return fail(c, DMSGM_ECUDA, "cudaSetDevice(%d) failed", c->device);
     cudaError_t e = cudaDeviceSynchronize();

@@ -31,9 +31,11 @@ EXPORTS = ("dmsgm_create", "dmsgm_step", "dmsgm_step_n", "dmsgm_step_host", "dms
            "dmsgm_set_band", "dmsgm_get_buffers", "dmsgm_attach_peer", "dmsgm_get_ipc_handles",
            "dmsgm_attach_peer_ipc", "dmsgm_band_signal", "dmsgm_band_wait", "dmsgm_band_sync",
            "dmsgm_get_status", "dmsgm_band_halo_needed", "dmsgm_set_prefilter", "dmsgm_prefilter",
-           "dmsgm_set_motion", "dmsgm_warp_frames")
+           "dmsgm_set_motion", "dmsgm_warp_frames", "dmsgm_set_mask_format")
 DMSGM_MC_MODELS = 0
 DMSGM_MC_FRAME = 1
+DMSGM_MASK_BYTES = 0
+DMSGM_MASK_BITS = 1
 DMSGM_IPC_BYTES = 192
 
 
@@ -98,6 +100,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.dmsgm_band_halo_needed.argtypes = [i32, i32, i32, P, i32, i32, i32, ctypes.POINTER(ctypes.c_int)]
     lib.dmsgm_set_prefilter.argtypes = [P, i32, ctypes.c_float, i32]
     lib.dmsgm_set_motion.argtypes = [P, i32]
+    lib.dmsgm_set_mask_format.argtypes = [P, i32]
     lib.dmsgm_warp_frames.argtypes = [i32, i32, i32, P, sz, P, P, sz, P]
     lib.dmsgm_prefilter.argtypes = [i32, i32, i32, P, sz, P, sz, i32, ctypes.c_float, i32, P]
     lib.dmsgm_version.argtypes = []
@@ -224,6 +227,7 @@ class Dmsgm:
             raise DmsgmError(rc, self._lib.dmsgm_last_error(None).decode())
         self._h = h
         self.device = device
+        self.mask_format = DMSGM_MASK_BYTES
         self.info = self.get_info()
 
     # -- helpers -------------------------------------------------------------
@@ -231,7 +235,8 @@ class Dmsgm:
         rows = self.info.band_rows * self.block            # pixel rows of a (band) image
         S = self.info.num_streams
         _check_tensor("frames", frames, (*lead, S, rows, self.width), "uint8", device, rows)
-        _check_tensor("masks", masks, (*lead, S, rows, self.width), "uint8", device, rows)
+        mw = (self.width + 7) // 8 if self.mask_format == DMSGM_MASK_BITS else self.width   # bytes per mask row
+        _check_tensor("masks", masks, (*lead, S, rows, mw), "uint8", device, rows)
         _check_tensor("homographies", homographies, (*lead, S, 9), "float64", device)
 
     def _check(self, rc: int):
@@ -304,6 +309,12 @@ class Dmsgm:
     def set_prefilter(self, gauss_size: int = 5, gauss_sigma: float = 1.0, median_radius: int = 1):
         self._check(self._lib.dmsgm_set_prefilter(self._h, gauss_size, gauss_sigma, median_radius))
         self.info = self.get_info()
+
+    def set_mask_format(self, fmt: int):
+        """DMSGM_MASK_BYTES (0, default: 0 / 255 per pixel) or DMSGM_MASK_BITS (1: one bit per
+        pixel, LSB first, masks [S][H][>= ceil(W/8)] bytes); see include/dmsgm.h."""
+        self._check(self._lib.dmsgm_set_mask_format(self._h, fmt))
+        self.mask_format = fmt
 
     def set_motion(self, mode: int):
         """DMSGM_MC_MODELS (0, default) or DMSGM_MC_FRAME (1, App. F frame warp)."""
