@@ -346,9 +346,14 @@ def run_dmsgm(args, rank, world, local):
     frames = ring.repeat(GRAPH_T // RING, 1, 1, 1)
     del ring
     Hs_dev = torch.from_numpy(np.ascontiguousarray(np.tile(Hs, (GRAPH_T // RING, 1, 1)))).to(dev)
-    masks = torch.empty_like(frames)
     params = method_params(dm, S)
     ctx = dm.Dmsgm(W, H, N, params, device=local)
+    if args.masks == "bits":
+        # DMSGM_MASK_BITS: the same decisions, one bit per pixel (include/dmsgm.h)
+        ctx.set_mask_format(dm.DMSGM_MASK_BITS)
+        masks = torch.empty((GRAPH_T, S, H, (W + 7) // 8), dtype=torch.uint8, device=dev)
+    else:
+        masks = torch.empty_like(frames)
     pf = None
     if args.prefilter:
         gs, sg, mr = args.prefilter.split(",")
@@ -428,6 +433,8 @@ def run_dmsgm(args, rank, world, local):
     # ---- end to end through the public API with HOST buffers (pinned) ----
     e2e = None
     if not args.no_e2e and klt is None:
+        if args.masks == "bits":
+            ctx.set_mask_format(dm.DMSGM_MASK_BYTES)    # e2e reports both formats below
         hf = torch.empty((S, H, W), dtype=torch.uint8, pin_memory=True)
         hm = torch.empty((S, H, W), dtype=torch.uint8, pin_memory=True)
         hH = torch.empty((RING, S, 9), dtype=torch.float64, pin_memory=True)
@@ -584,14 +591,16 @@ def run_dmsgm(args, rank, world, local):
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth/ ring recipe, generated on device)",
             "config": {"workload": args.config + ("+prefilter" if pf else "") +
-                                   {"frame": "+framewarp", "estimate": "+klt"}.get(args.motion, ""),
+                                   {"frame": "+framewarp", "estimate": "+klt"}.get(args.motion, "") +
+                                   ("+bitmasks" if args.masks == "bits" else ""),
+                       "mask_format": args.masks,
                        "desc": wl["desc"], "W": W, "H": H, "motion_compensation": args.motion,
                        "N": N, "prefilter": {"gauss_size": pf[0], "gauss_sigma": pf[1], "median_radius": pf[2]}
                        if pf else None,
                        "streams_per_gpu": S, "total_streams": total_streams, "ring_frames": RING,
                        "l2": f"inputs larger than L2: {bytes_per_step / 1e6:.1f} MB algorithmic traffic per step; "
                              f"{GRAPH_T} frame + mask slots per stream ({RING} distinct frames repeated), "
-                             f"{2 * GRAPH_T * S * W * H / 1e9:.2f} GB",
+                             f"{(frames.numel() + masks.numel()) / 1e9:.2f} GB",
                        "parallelism": f"stream-sharded x{world}, no data-path collective"},
             "mpixel_per_s": fps * W * H / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -837,6 +846,8 @@ def main():
                     help="timed steps as dmsgm_step_n graph replays (default) or single dmsgm_step launches (A/B)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--masks", default="bytes", choices=["bytes", "bits"],
+                    help="mask output of the timed steps: 0/255 bytes (default) or DMSGM_MASK_BITS")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=0,
                     help="override streams per GPU (profiling only; the bench workload is the config's)")

@@ -75,7 +75,8 @@ typedef struct {
     int band_row0, band_rows, band_halo; /* row band (0, Hb, 0 for the whole frame)    */
     size_t state_bytes;            /* one state buffer (internal chunk-SoA layout, padded to Wb%4) */
     double algorithmic_bytes_per_frame; /* frame read + mask write + state read+write, one stream
-                                           (band: its rows + the halo rows sent to neighbours) */
+                                           (band: its rows + the halo rows sent to neighbours;
+                                           DMSGM_MASK_BITS: the mask write is ceil(W/8) B/row) */
     char kernel[64];               /* the kernel dmsgm_step launches, e.g. "dmsgm_step_staged<4,2>" */
 } dmsgm_info;
 

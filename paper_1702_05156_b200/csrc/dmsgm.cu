@@ -921,14 +921,16 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     // frame read (1 B/px) + mask write (1 B/px) + state read + write (2 x 24 B per block)
     // (band mode: the band's rows, plus the halo rows stored into each neighbour)
     const int nb = (c->peer_slot[0] ? 1 : 0) + (c->peer_slot[1] ? 1 : 0);
-    out->algorithmic_bytes_per_frame = 2.0 * c->W * c->Hp + 2.0 * 24.0 * (double)c->Wb * c->rows +
+    // (DMSGM_MASK_BITS: the mask write is ceil(W/8) B per row)
+    const double mask_row = c->mask_bits ? (double)((c->W + 7) / 8) : (double)c->W;
+    out->algorithmic_bytes_per_frame = ((double)c->W + mask_row) * c->Hp + 2.0 * 24.0 * (double)c->Wb * c->rows +
                                        24.0 * (double)c->Wb * c->halo * nb;
     // preprocessing as its own kernel: + read the frame + write the filtered frame
     if (c->pf_buf) out->algorithmic_bytes_per_frame += 2.0 * c->W * c->Hp;
     if (c->wf_buf) out->algorithmic_bytes_per_frame += 2.0 * c->W * c->Hp;     // frame warp: read + write
     if (c->staged)
-        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d> (TMA, persistent)", c->N,
-                 c->N == 8 ? 1 : 2, c->staged_occ);
+        snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d%s> (TMA, persistent)", c->N,
+                 c->N == 8 ? 1 : 2, c->staged_occ, c->mask_bits ? ",bits" : "");
     else
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_kernel<%d,%d>", c->N, bpt_of(c));
     if (c->staged && c->band)
