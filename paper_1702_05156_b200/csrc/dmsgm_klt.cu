@@ -163,7 +163,8 @@ cudaError_t launch_ransac(dmsgm_klt_ctx* c, const double* src, const double* dst
     RansacArgs r;
     r.src = src; r.dst = dst; r.mcount = mcount; r.max_corners = c->p.max_corners; r.iters = c->p.ransac_iters;
     r.seed = c->p.seed; r.thresh2 = c->p.ransac_thresh * c->p.ransac_thresh; r.iter_counts = iter_counts;
-    klt_ransac_kernel<<<dim3((c->p.ransac_iters + 3) / 4, c->S), 128, 0, st>>>(r);
+    klt_ransac_kernel<<<dim3((c->p.ransac_iters + kRansacWarps * kRansacPerWarp - 1) / (kRansacWarps * kRansacPerWarp), c->S),
+                        32 * kRansacWarps, 0, st>>>(r);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     RefitArgs f;

@@ -12,8 +12,8 @@
 //   klt_pyramid_kernel  all box-pyramid levels of prev and next in one pass (R39)
 //   klt_lk_kernel       one warp per corner, pyramidal Lucas-Kanade in fp32 (R40)
 //   klt_compact_kernel  tracked pairs -> RANSAC matches (f64), one warp per stream
-//   klt_ransac_kernel   one warp per (stream, iteration): SplitMix64 sample, 8x8 fp64
-//                       solve, inlier count (R42)
+//   klt_ransac_kernel   one warp per (stream, 4 iterations): SplitMix64 sample, 8x8 fp64
+//                       solve row-parallel on 8 lanes, inlier count (R42)
 //   klt_refit_kernel    one warp per stream: best model, its inliers, normalized DLT by
 //                       the smallest eigenvector of A^T A (inverse iteration, fp64) (R41)
 #pragma once
@@ -853,7 +853,7 @@ __global__ void klt_compact_kernel(const CompactArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// K6: RANSAC hypotheses (R42), one warp per (stream, iteration)
+// K6: RANSAC hypotheses (R42), one warp per (stream, 4 iterations)
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
     z += 0x9E3779B97F4A7C15ull;
@@ -946,31 +946,106 @@ struct RansacArgs {
     int* iter_counts;     // [S][iters]
 };
 
-__global__ void __launch_bounds__(128) klt_ransac_kernel(const RansacArgs a) {
-    const int it = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31, s = blockIdx.y;
-    if (it >= a.iters) return;
+// One warp per 4 iterations: lanes 8g .. 8g+7 hold the 8 rows of iteration 4w+g's 8x8
+// system (row r: its 9 coefficients), so the elimination runs row-parallel -- per column the
+// pivot by a 3-step (value, lower row) max within the 8 lanes, the row swap and the pivot
+// row by shuffles, each row's f = A[r][c] / A[c][c] and update on its own lane -- with
+// exactly minimal_h's operations on every entry (the same pivots, quotients, products and
+// differences in the same order: the same h, bit for bit).  Then each group counts its
+// hypothesis' inliers over the matches (8 lanes).  Replaces one warp per iteration in which
+// all 32 lanes repeated one serial solve (~70 % of its instructions).
+constexpr int kRansacWarps = 4;
+constexpr int kRansacPerWarp = 4;
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+    return __hiloint2double(__shfl_sync(0xffffffffu, __double2hiint(v), src),
+                            __shfl_sync(0xffffffffu, __double2loint(v), src));
+}
+__device__ __forceinline__ double shfl_xor_d(double v, int m) {
+    return __hiloint2double(__shfl_xor_sync(0xffffffffu, __double2hiint(v), m),
+                            __shfl_xor_sync(0xffffffffu, __double2loint(v), m));
+}
+
+__global__ void __launch_bounds__(32 * kRansacWarps) klt_ransac_kernel(const RansacArgs a) {
+    const int w = blockIdx.x * kRansacWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31, s = blockIdx.y;
+    if (w * kRansacPerWarp >= a.iters) return;                     // warp-uniform
+    const int g = lane >> 3, r = lane & 7, base = lane & ~7;       // group (iteration) and row
+    const int it = w * kRansacPerWarp + g;
     const int n = a.mcount[s];
     const double* src = a.src + (long long)s * a.max_corners * 2;
     const double* dst = a.dst + (long long)s * a.max_corners * 2;
-    int result = -1;
     int idx[4];
-    double h[9];
-    if (n >= 4 && ransac_sample(a.seed, it, n, idx)) {
+    bool ok = it < a.iters && n >= 4 && ransac_sample(a.seed, it, n, idx);
+    double xs = 0.0, ys = 0.0, us = 0.0, vs = 0.0;                  // this row's correspondence
+    if (ok) {
         double x[4], y[4], u[4], v[4];
         for (int k = 0; k < 4; ++k) {
             x[k] = src[2 * idx[k]]; y[k] = src[2 * idx[k] + 1];
             u[k] = dst[2 * idx[k]]; v[k] = dst[2 * idx[k] + 1];
         }
-        if (minimal_h(x, y, u, v, h)) {
-            int c = 0;
-            for (int j = lane; j < n; j += 32)
-                c += reproj_err2(h, src[2 * j], src[2 * j + 1], dst[2 * j], dst[2 * j + 1]) < a.thresh2;
+        ok = !collinear4(x, y) && !collinear4(u, v);
+        const int i = r >> 1;
+        xs = i == 0 ? x[0] : i == 1 ? x[1] : i == 2 ? x[2] : x[3];
+        ys = i == 0 ? y[0] : i == 1 ? y[1] : i == 2 ? y[2] : y[3];
+        us = i == 0 ? u[0] : i == 1 ? u[1] : i == 2 ? u[2] : u[3];
+        vs = i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3];
+    }
+    // row r of minimal_h's system: even r = 2i: (x, y, 1, 0, 0, 0, -u x, -u y, u);
+    // odd r = 2i+1: (0, 0, 0, x, y, 1, -v x, -v y, v)
+    const bool odd = r & 1;
+    const double t = odd ? vs : us;
+    double A[9];
+    A[0] = odd ? 0.0 : xs; A[1] = odd ? 0.0 : ys; A[2] = odd ? 0.0 : 1.0;
+    A[3] = odd ? xs : 0.0; A[4] = odd ? ys : 0.0; A[5] = odd ? 1.0 : 0.0;
+    A[6] = -__dmul_rn(t, xs); A[7] = -__dmul_rn(t, ys); A[8] = t;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-            result = c;
+    for (int c = 0; c < 8; ++c) {
+        // pivot: the first row >= c of the largest |A[r][c]| (minimal_h's strict '>' scan from
+        // row c: a NaN row below c never wins; a NaN at row c fails the sample)
+        const double av = fabs(A[c]);
+        const bool nan_c = __shfl_sync(0xffffffffu, (int)(av != av), base + c) != 0;
+        double kv = r < c ? -2.0 : (r == c ? av : (av != av ? -1.0 : av));
+        int kr = r;
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1) {
+            const double ov = shfl_xor_d(kv, m);
+            const int orow = __shfl_xor_sync(0xffffffffu, kr, m);
+            if (ov > kv || (ov == kv && orow < kr)) { kv = ov; kr = orow; }
+        }
+        ok = ok && !nan_c && kv > 0.0;
+        const int piv = kr;
+        // swap rows c and piv (columns c .. 8; the columns left of c are never read again)
+        const int from = r == c ? piv : (r == piv ? c : r);
+#pragma unroll
+        for (int k = c; k < 9; ++k) A[k] = shfl_d(A[k], base + from);
+        // eliminate below the pivot row
+        double P[9];
+#pragma unroll
+        for (int k = c; k < 9; ++k) P[k] = shfl_d(A[k], base + c);
+        if (r > c) {
+            const double f = __ddiv_rn(A[c], P[c]);
+#pragma unroll
+            for (int k = c + 1; k < 9; ++k) A[k] = __dsub_rn(A[k], __dmul_rn(f, P[k]));
         }
     }
-    if (lane == 0) a.iter_counts[(long long)s * a.iters + it] = result;
+    // back substitution, h[8] = 1: row r on lane r, h broadcast as it is found
+    double h[9];
+    h[8] = 1.0;
+#pragma unroll
+    for (int rr = 7; rr >= 0; --rr) {
+        double acc = A[8];
+#pragma unroll
+        for (int k = rr + 1; k < 8; ++k) acc = __dsub_rn(acc, __dmul_rn(A[k], h[k]));
+        h[rr] = shfl_d(__ddiv_rn(acc, A[rr]), base + rr);
+    }
+    // inliers of this group's hypothesis over the matches, 8 lanes
+    int cnt = 0;
+    if (ok)
+        for (int j = r; j < n; j += 8)
+            cnt += reproj_err2(h, src[2 * j], src[2 * j + 1], dst[2 * j], dst[2 * j + 1]) < a.thresh2;
+#pragma unroll
+    for (int m = 4; m > 0; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
+    if (r == 0 && it < a.iters) a.iter_counts[(long long)s * a.iters + it] = ok ? cnt : -1;
 }
 
 // ---------------------------------------------------------------------------------------
