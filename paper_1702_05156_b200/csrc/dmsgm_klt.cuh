@@ -21,7 +21,15 @@
 #include <limits.h>
 #include <stdint.h>
 
+#include "dmsgm_pair.cuh"     // paired fp32 (FFMA2 / FMUL2 / FADD2)
+
 namespace dmsgm_klt {
+
+using dmsgm::f2_add;
+using dmsgm::f2_bc;
+using dmsgm::f2_fma;
+using dmsgm::f2_mul;
+using dmsgm::f2_sub;
 
 constexpr int kMaxLevels = 6;        // levels 0..5
 constexpr int kMaxCorners = 1024;
@@ -619,6 +627,9 @@ constexpr int kLkMaxWin = 32;
 #ifndef DMSGM_LK_MINB
 #define DMSGM_LK_MINB 3
 #endif
+#ifndef DMSGM_LK_PAIRED
+#define DMSGM_LK_PAIRED 1
+#endif
 constexpr int kLkMargin = 4;     // next-image region: the window +- this many pixels of flow per level
 
 template <int NS>   // samples per lane: ceil(win^2 / 32)
@@ -762,6 +773,35 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
                 // lane's padding samples (q >= win^2) read offset 0 and have I = Ix = Iy = 0, so
                 // they add exactly +0 to both sums
                 const float* base = region + dyr * rs + dxr;
+#if DMSGM_LK_PAIRED
+                // two samples per paired instruction (FFMA2 / FMUL2 / FADD2), the blend and
+                // the sums as fmas: ~4.5 FP instructions per sample instead of 12 (LK is
+                // compared with the oracle within a tolerance, not bitwise)
+                const float2 GXW = f2_bc(gxw), FX = f2_bc(fx), GYW = f2_bc(gyw), FY = f2_bc(fy);
+                float2 bx2 = f2_bc(0.0f), by2 = f2_bc(0.0f);
+#pragma unroll
+                for (int k = 0; k + 1 < NS; k += 2) {
+                    const float* ra = base + roff[k];
+                    const float* rb = base + roff[k + 1];
+                    const float2 p00 = make_float2(ra[0], rb[0]), p10 = make_float2(ra[1], rb[1]);
+                    const float2 p01 = make_float2(ra[rs], rb[rs]), p11 = make_float2(ra[rs + 1], rb[rs + 1]);
+                    const float2 top = f2_fma(p00, GXW, f2_mul(p10, FX));
+                    const float2 bot = f2_fma(p01, GXW, f2_mul(p11, FX));
+                    const float2 e = f2_sub(make_float2(I[k], I[k + 1]), f2_fma(top, GYW, f2_mul(bot, FY)));
+                    bx2 = f2_fma(e, make_float2(Ix[k], Ix[k + 1]), bx2);
+                    by2 = f2_fma(e, make_float2(Iy[k], Iy[k + 1]), by2);
+                }
+                bx = __fadd_rn(bx2.x, bx2.y);
+                by = __fadd_rn(by2.x, by2.y);
+                if constexpr (NS & 1) {
+                    const float* r0 = base + roff[NS - 1];
+                    const float top = __fmaf_rn(r0[0], gxw, __fmul_rn(r0[1], fx));
+                    const float bot = __fmaf_rn(r0[rs], gxw, __fmul_rn(r0[rs + 1], fx));
+                    const float e = __fsub_rn(I[NS - 1], __fmaf_rn(top, gyw, __fmul_rn(bot, fy)));
+                    bx = __fmaf_rn(e, Ix[NS - 1], bx);
+                    by = __fmaf_rn(e, Iy[NS - 1], by);
+                }
+#else
 #pragma unroll
                 for (int k = 0; k < NS; ++k) {
                     const float* r0 = base + roff[k];
@@ -772,6 +812,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
                     bx = __fadd_rn(bx, __fmul_rn(e, Ix[k]));
                     by = __fadd_rn(by, __fmul_rn(e, Iy[k]));
                 }
+#endif
             } else {
 #pragma unroll
                 for (int k = 0; k < NS; ++k) {
