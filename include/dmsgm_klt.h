@@ -73,6 +73,24 @@ int dmsgm_klt_create(int width, int height, const dmsgm_klt_params* p, int devic
 int dmsgm_klt_estimate(dmsgm_klt_ctx* ctx, const uint8_t* prev, size_t prev_pitch, const uint8_t* next,
                        size_t next_pitch, double* H_out, int* ok_out, void* cuda_stream);
 
+/* The same estimate for consecutive frame pairs of a video (App. F runs the chain once per
+ * frame): identical H_out / ok_out to dmsgm_klt_estimate(prev, next).  When
+ * `prev` is the buffer (same pointer and pitch) passed as `next` to the previous
+ * dmsgm_klt_estimate_seq call on this context, and no other dmsgm_klt_* call that computes
+ * corners or pyramids (estimate, corners, track) or dmsgm_klt_seq_reset came in between,
+ * the corners and pyramid levels computed from that frame are reused -- the CALLER
+ * guarantees the buffer's content is unchanged since that call (else call
+ * dmsgm_klt_seq_reset first).  Otherwise everything is computed from `prev` as in
+ * dmsgm_klt_estimate.  The corners of `next` (for the following call) are computed on an
+ * internal stream beside this pair's tracking and fit, and joined back into `cuda_stream`
+ * before the call's work ends there.  7 kernel launches (9 when prev is not cached), no
+ * host synchronisation; errors as dmsgm_klt_estimate (the cache is dropped on any error). */
+int dmsgm_klt_estimate_seq(dmsgm_klt_ctx* ctx, const uint8_t* prev, size_t prev_pitch, const uint8_t* next,
+                           size_t next_pitch, double* H_out, int* ok_out, void* cuda_stream);
+
+/* Forget the frame dmsgm_klt_estimate_seq cached (the next call recomputes from `prev`). */
+int dmsgm_klt_seq_reset(dmsgm_klt_ctx* ctx);
+
 /* Stage 1 alone (R38): corners_out int32 [S][max_corners][2] (x, y pixel indices, in
  * selection order), counts_out int32 [S]. */
 int dmsgm_klt_corners(dmsgm_klt_ctx* ctx, const uint8_t* frames, size_t pitch, int* corners_out,

@@ -35,8 +35,8 @@ struct dmsgm_klt_ctx {
     uint16_t* grid_global;           // [S][gh][gw] or null (grid in shared memory)
     int cell, gw, gh;
     size_t sel_smem;
-    int* corners;                    // [S][max][2]
-    int* counts;                     // [S]
+    int* corners;                    // [2][S][max][2] (slot 1: dmsgm_klt_estimate_seq only)
+    int* counts;                     // [2][S]
     float* tracked;                  // [S][max][2]
     uint8_t* status;                 // [S][max]
     double* src;                     // [S][max][2]
@@ -47,6 +47,12 @@ struct dmsgm_klt_ctx {
     // the corner score / select kernels, and joins before LK
     cudaStream_t side;
     cudaEvent_t ev_fork, ev_pyr;
+    // dmsgm_klt_estimate_seq: the frame last passed as `next` (pointer, pitch), the pyramid set
+    // and the corner slot that hold its levels and corners
+    bool seq_valid;
+    const uint8_t* seq_ptr;
+    size_t seq_pitch;
+    int seq_set, seq_slot;
     char err[512];
 };
 
@@ -122,29 +128,48 @@ cudaError_t launch_corners(dmsgm_klt_ctx* c, const uint8_t* frames, size_t pitch
     return cudaGetLastError();
 }
 
-cudaError_t launch_track(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, const uint8_t* next, size_t npitch,
-                         const int* corners, const int* counts, float* tracked, uint8_t* status, cudaStream_t st,
-                         bool skip_pyramid = false) {
-    cudaError_t e;
+// Pyramid levels 1.. of n = 1 or 2 images (each S streams) into pyramid sets dset[i].
+cudaError_t launch_pyramid(dmsgm_klt_ctx* c, int n, const uint8_t* const* img, const size_t* pitch, const int* dset,
+                           cudaStream_t st) {
+    if (c->nlev <= 1) return cudaSuccess;
     PyrArgs pa;
-    pa.img0[0] = prev; pa.img0[1] = next;
-    pa.stride0[0] = (long long)c->H * (long long)ppitch; pa.stride0[1] = (long long)c->H * (long long)npitch;
-    pa.pitch0[0] = (int)ppitch; pa.pitch0[1] = (int)npitch;
+    for (int i = 0; i < 2; ++i) {
+        const int j = i < n ? i : 0;
+        pa.img0[i] = img[j];
+        pa.stride0[i] = (long long)c->H * (long long)pitch[j];
+        pa.pitch0[i] = (int)pitch[j];
+        pa.dset[i] = dset[j];
+        pa.vec[i] = ((uintptr_t)img[j] & 15) == 0 && (pitch[j] & 15) == 0;
+    }
     for (int L = 0; L < kMaxLevels; ++L) { pa.lev[L] = c->pyr[L]; pa.w[L] = c->lw[L]; pa.h[L] = c->lh[L]; }
     pa.nlev = c->nlev; pa.S = c->S;
-    if (c->nlev > 1 && !skip_pyramid) {
-        klt_pyramid_kernel<<<dim3((c->lw[1] + 15) / 16, (c->lh[1] + 15) / 16, 2 * c->S), 256, 0, st>>>(pa);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    klt_pyramid_kernel<<<dim3((c->lw[1] + kPyrTX - 1) / kPyrTX, (c->lh[1] + kPyrTY - 1) / kPyrTY, n * c->S), 256, 0,
+                         st>>>(pa);
+    return cudaGetLastError();
+}
+
+// LK of corners from prev (pyramid set pset) to next (set nset); skip_pyramid: the levels
+// are already built, else both images' levels are built here into sets 0 / 1
+cudaError_t launch_track(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, const uint8_t* next, size_t npitch,
+                         const int* corners, const int* counts, float* tracked, uint8_t* status, cudaStream_t st,
+                         bool skip_pyramid = false, int pset = 0, int nset = 1) {
+    cudaError_t e;
+    if (!skip_pyramid) {
+        const uint8_t* img[2] = {prev, next};
+        const size_t pit[2] = {ppitch, npitch};
+        const int ds[2] = {0, 1};
+        if ((e = launch_pyramid(c, 2, img, pit, ds, st)) != cudaSuccess) return e;
+        pset = 0; nset = 1;
     }
     LkArgs la;
     for (int L = 0; L < kMaxLevels; ++L) {
         if (L == 0) {
-            la.prev[0] = Img{prev, pa.stride0[0], (int)ppitch, c->W, c->H};
-            la.next[0] = Img{next, pa.stride0[1], (int)npitch, c->W, c->H};
+            la.prev[0] = Img{prev, (long long)c->H * (long long)ppitch, (int)ppitch, c->W, c->H};
+            la.next[0] = Img{next, (long long)c->H * (long long)npitch, (int)npitch, c->W, c->H};
         } else {
             const long long img = (long long)c->lw[L] * c->lh[L];
-            la.prev[L] = Img{c->pyr[L], img, c->lw[L], c->lw[L], c->lh[L]};
-            la.next[L] = Img{c->pyr[L] ? c->pyr[L] + img * c->S : nullptr, img, c->lw[L], c->lw[L], c->lh[L]};
+            la.prev[L] = Img{c->pyr[L] ? c->pyr[L] + img * c->S * pset : nullptr, img, c->lw[L], c->lw[L], c->lh[L]};
+            la.next[L] = Img{c->pyr[L] ? c->pyr[L] + img * c->S * nset : nullptr, img, c->lw[L], c->lw[L], c->lh[L]};
         }
     }
     la.nlev = c->nlev; la.win = c->p.win; la.max_iters = c->p.max_iters; la.max_corners = c->p.max_corners;
@@ -217,8 +242,8 @@ int dmsgm_klt_create(int width, int height, const dmsgm_klt_params* p, int devic
     KALLOC(c->cand, (size_t)S * c->cap * sizeof(unsigned long long));
     KALLOC(c->cand_count, 2 * (size_t)S * sizeof(unsigned));
     KALLOC(c->overflow, sizeof(unsigned));
-    KALLOC(c->corners, (size_t)S * M * 2 * sizeof(int));
-    KALLOC(c->counts, (size_t)S * sizeof(int));
+    KALLOC(c->corners, 2 * (size_t)S * M * 2 * sizeof(int));
+    KALLOC(c->counts, 2 * (size_t)S * sizeof(int));
     KALLOC(c->tracked, (size_t)S * M * 2 * sizeof(float));
     KALLOC(c->status, (size_t)S * M);
     KALLOC(c->src, (size_t)S * M * 2 * sizeof(double));
@@ -249,6 +274,7 @@ int dmsgm_klt_corners(dmsgm_klt_ctx* c, const uint8_t* frames, size_t pitch, int
     if (!c) return DMSGM_EINVAL;
     if (!img_ok(c, frames, pitch) || !corners_out || !counts_out) return kfail(c, DMSGM_EINVAL, "bad frames / outputs");
     Dev g(c->device);
+    c->seq_valid = false;                        // the candidate buffers are shared
     cudaError_t e = launch_corners(c, frames, pitch, corners_out, counts_out, (cudaStream_t)stream);
     if (e != cudaSuccess) return kcuda(c, e, "dmsgm_klt_corners");
     return DMSGM_OK;
@@ -260,6 +286,7 @@ int dmsgm_klt_track(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, const 
     if (!img_ok(c, prev, ppitch) || !img_ok(c, next, npitch) || !corners || !counts || !tracked_out || !status_out)
         return kfail(c, DMSGM_EINVAL, "bad frames / corners / outputs");
     Dev g(c->device);
+    c->seq_valid = false;                        // both pyramid sets are overwritten
     cudaError_t e = launch_track(c, prev, ppitch, next, npitch, corners, counts, tracked_out, status_out,
                                  (cudaStream_t)stream);
     if (e != cudaSuccess) return kcuda(c, e, "dmsgm_klt_track");
@@ -278,12 +305,29 @@ int dmsgm_klt_ransac(dmsgm_klt_ctx* c, const double* src, const double* dst, con
     return DMSGM_OK;
 }
 
+namespace {
+// compact -> RANSAC -> refit of the tracked pairs (corners / counts of the tracked slot)
+cudaError_t launch_fit(dmsgm_klt_ctx* c, const int* corners, const int* counts, double* H_out, int* ok_out,
+                       cudaStream_t st) {
+    CompactArgs ca;
+    ca.corners = corners; ca.counts = counts; ca.tracked = c->tracked; ca.status = c->status;
+    ca.max_corners = c->p.max_corners; ca.S = c->S; ca.src = c->src; ca.dst = c->dst; ca.mcount = c->mcount;
+    klt_compact_kernel<<<(c->S + 3) / 4, 128, 0, st>>>(ca);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = launch_ransac(c, c->src, c->dst, c->mcount, H_out, nullptr, c->iter_counts, ok_out, st);
+    return e;
+}
+int* slot_corners(dmsgm_klt_ctx* c, int slot) { return c->corners + (size_t)slot * c->S * c->p.max_corners * 2; }
+int* slot_counts(dmsgm_klt_ctx* c, int slot) { return c->counts + (size_t)slot * c->S; }
+}  // namespace
+
 int dmsgm_klt_estimate(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, const uint8_t* next, size_t npitch,
                        double* H_out, int* ok_out, void* stream) {
     if (!c) return DMSGM_EINVAL;
     if (!img_ok(c, prev, ppitch) || !img_ok(c, next, npitch) || !H_out || ((uintptr_t)H_out & 7))
         return kfail(c, DMSGM_EINVAL, "bad frames / outputs");
     Dev g(c->device);
+    c->seq_valid = false;                        // slot 0 and both pyramid sets are overwritten
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
     // the pyramid of prev and next on the side stream, forked after the score kernel so that it
@@ -293,29 +337,69 @@ int dmsgm_klt_estimate(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, con
         cudaError_t fe = cudaEventRecord(c->ev_fork, st);
         if (fe == cudaSuccess) fe = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
         if (fe != cudaSuccess) return fe;
-        PyrArgs pa;
-        pa.img0[0] = prev; pa.img0[1] = next;
-        pa.stride0[0] = (long long)c->H * (long long)ppitch; pa.stride0[1] = (long long)c->H * (long long)npitch;
-        pa.pitch0[0] = (int)ppitch; pa.pitch0[1] = (int)npitch;
-        for (int L = 0; L < kMaxLevels; ++L) { pa.lev[L] = c->pyr[L]; pa.w[L] = c->lw[L]; pa.h[L] = c->lh[L]; }
-        pa.nlev = c->nlev; pa.S = c->S;
-        klt_pyramid_kernel<<<dim3((c->lw[1] + 15) / 16, (c->lh[1] + 15) / 16, 2 * c->S), 256, 0, c->side>>>(pa);
-        if ((fe = cudaGetLastError()) != cudaSuccess) return fe;
+        const uint8_t* img[2] = {prev, next};
+        const size_t pit[2] = {ppitch, npitch};
+        const int ds[2] = {0, 1};
+        if ((fe = launch_pyramid(c, 2, img, pit, ds, c->side)) != cudaSuccess) return fe;
         return cudaEventRecord(c->ev_pyr, c->side);
     };
     if (e == cudaSuccess) e = launch_corners(c, prev, ppitch, c->corners, c->counts, st, fork_pyramid);
     if (e == cudaSuccess && c->nlev > 1) e = cudaStreamWaitEvent(st, c->ev_pyr, 0);
     if (e == cudaSuccess)
         e = launch_track(c, prev, ppitch, next, npitch, c->corners, c->counts, c->tracked, c->status, st, true);
-    if (e == cudaSuccess) {
-        CompactArgs ca;
-        ca.corners = c->corners; ca.counts = c->counts; ca.tracked = c->tracked; ca.status = c->status;
-        ca.max_corners = c->p.max_corners; ca.S = c->S; ca.src = c->src; ca.dst = c->dst; ca.mcount = c->mcount;
-        klt_compact_kernel<<<(c->S + 3) / 4, 128, 0, st>>>(ca);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = launch_ransac(c, c->src, c->dst, c->mcount, H_out, nullptr, c->iter_counts, ok_out, st);
+    if (e == cudaSuccess) e = launch_fit(c, c->corners, c->counts, H_out, ok_out, st);
     if (e != cudaSuccess) return kcuda(c, e, "dmsgm_klt_estimate");
+    return DMSGM_OK;
+}
+
+int dmsgm_klt_estimate_seq(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, const uint8_t* next, size_t npitch,
+                           double* H_out, int* ok_out, void* stream) {
+    if (!c) return DMSGM_EINVAL;
+    if (!img_ok(c, prev, ppitch) || !img_ok(c, next, npitch) || !H_out || ((uintptr_t)H_out & 7))
+        return kfail(c, DMSGM_EINVAL, "bad frames / outputs");
+    Dev g(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    const bool cached = c->seq_valid && c->seq_ptr == prev && c->seq_pitch == ppitch;
+    c->seq_valid = false;
+    const int pset = cached ? c->seq_set : 0, pslot = cached ? c->seq_slot : 0;
+    const int nset = 1 - pset, nslot = 1 - pslot;
+    if (!cached) {
+        // first frame of a sequence (or a jump): corners and levels of prev, then next's levels
+        const uint8_t* img[2] = {prev, next};
+        const size_t pit[2] = {ppitch, npitch};
+        const int ds[2] = {pset, nset};
+        e = launch_corners(c, prev, ppitch, slot_corners(c, pslot), slot_counts(c, pslot), st);
+        if (e == cudaSuccess) e = launch_pyramid(c, 2, img, pit, ds, st);
+    } else {
+        const uint8_t* img[1] = {next};
+        const size_t pit[1] = {npitch};
+        const int ds[1] = {nset};
+        e = launch_pyramid(c, 1, img, pit, ds, st);
+    }
+    // the corners of next (the next call's prev) on the side stream, beside LK and the fit of
+    // this pair; joined at the end, so the call's work is complete when `cuda_stream` is
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    if (e == cudaSuccess) e = launch_corners(c, next, npitch, slot_corners(c, nslot), slot_counts(c, nslot), c->side);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_pyr, c->side);
+    if (e == cudaSuccess)
+        e = launch_track(c, prev, ppitch, next, npitch, slot_corners(c, pslot), slot_counts(c, pslot), c->tracked,
+                         c->status, st, true, pset, nset);
+    if (e == cudaSuccess) e = launch_fit(c, slot_corners(c, pslot), slot_counts(c, pslot), H_out, ok_out, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c->ev_pyr, 0);
+    if (e != cudaSuccess) return kcuda(c, e, "dmsgm_klt_estimate_seq");
+    c->seq_valid = true;
+    c->seq_ptr = next;
+    c->seq_pitch = npitch;
+    c->seq_set = nset;
+    c->seq_slot = nslot;
+    return DMSGM_OK;
+}
+
+int dmsgm_klt_seq_reset(dmsgm_klt_ctx* c) {
+    if (!c) return DMSGM_EINVAL;
+    c->seq_valid = false;
     return DMSGM_OK;
 }
 

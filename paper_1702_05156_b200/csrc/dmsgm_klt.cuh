@@ -9,7 +9,7 @@
 //   klt_select_kernel   one CTA per stream: exact top-2048 of the qualifying keys by an
 //                       8-pass radix select, bitonic sort in shared memory, greedy
 //                       min-distance selection by one warp over a cell grid (R38)
-//   klt_pyramid_kernel  all box-pyramid levels of prev and next in one pass (R39)
+//   klt_pyramid_kernel  all box-pyramid levels of prev and next in one pass, 16-byte rows (R39)
 //   klt_lk_kernel       one warp per corner, pyramidal Lucas-Kanade in fp32 (R40)
 //   klt_compact_kernel  tracked pairs -> RANSAC matches (f64), one warp per stream
 //   klt_ransac_kernel   one warp per (stream, 4 iterations): SplitMix64 sample, 8x8 fp64
@@ -525,45 +525,96 @@ __global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArg
 }
 
 // ---------------------------------------------------------------------------------------
-// K3: box pyramid levels 1..nlev-1 of prev (set 0) and next (set 1) in one pass (R39)
+// K3: box pyramid levels 1..nlev-1 of one or two images per stream (R39), all levels in one
+// pass.  A CTA owns a 32 x 64 tile of level 1 (64 x 128 pixels of level 0; 16 x 32 of level
+// 2, ... 2 x 4 of level 5).  Level 1: a thread averages 8 consecutive level-1 pixels from two
+// 16-byte level-0 row loads on 16-bit lanes (exact: the 2x2 sum + 2 <= 1022 fits a lane), one
+// 8-byte store; levels >= 2 from the previous level's tile in shared memory.  Partial chunks
+// (frame edges, unaligned frames) take the per-pixel path -- the same integers.
 // ---------------------------------------------------------------------------------------
 struct PyrArgs {
     const uint8_t* img0[2];
     long long stride0[2];
     int pitch0[2];
-    uint8_t* lev[kMaxLevels];      // level L >= 1: [2][S][h_L][w_L]
+    int dset[2];                   // destination set of image i (level L >= 1: [2][S][h_L][w_L])
+    int vec[2];                    // level-0 rows 16-byte aligned (base and pitch)
+    uint8_t* lev[kMaxLevels];
     int w[kMaxLevels], h[kMaxLevels];
     int nlev, S;
 };
 
+constexpr int kPyrTX = 64, kPyrTY = 32;   // level-1 tile
+
+__device__ __forceinline__ uint32_t pyr_avg2(uint32_t a, uint32_t b) {
+    // bytes (a0 a1 a2 a3) of row 2y, (b0 b1 b2 b3) of row 2y+1 -> level-1 pixels
+    // (a0+a1+b0+b1+2)>>2 in byte 0 and (a2+a3+b2+b3+2)>>2 in byte 2
+    const uint32_t e = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu) + (b & 0x00FF00FFu) + ((b >> 8) & 0x00FF00FFu) +
+                       0x00020002u;
+    return (e >> 2) & 0x00FF00FFu;
+}
+
 __global__ void __launch_bounds__(256) klt_pyramid_kernel(const PyrArgs a) {
-    __shared__ int t[2][16][16];
+    __shared__ __align__(16) uint8_t t1[kPyrTY][kPyrTX];
+    __shared__ uint8_t t2[kPyrTY / 2][kPyrTX / 2];
     const int z = blockIdx.z, set = z / a.S, s = z - set * a.S;
+    const long long zd = (long long)a.dset[set] * a.S + s;        // destination image index
     const uint8_t* src = a.img0[set] + (long long)s * a.stride0[set];
     const int p0 = a.pitch0[set];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    int cur = 0;
+    const int tid = threadIdx.x;
     {
-        const int x = blockIdx.x * 16 + tx, y = blockIdx.y * 16 + ty;
-        int v = 0;
-        if (x < a.w[1] && y < a.h[1]) {
+        // level 1: thread = 8 consecutive pixels of one row of the tile
+        const int ty = tid >> 3, tx = (tid & 7) * 8;
+        const int y = blockIdx.y * kPyrTY + ty, x = blockIdx.x * kPyrTX + tx;
+        const int w1 = a.w[1], h1 = a.h[1];
+        uint32_t lo = 0, hi = 0;
+        if (y < h1) {
             const uint8_t* r0 = src + (long long)(2 * y) * p0 + 2 * x;
-            v = (r0[0] + r0[1] + r0[p0] + r0[p0 + 1] + 2) >> 2;
-            a.lev[1][((long long)z * a.h[1] + y) * a.w[1] + x] = (uint8_t)v;
+            uint8_t* o = a.lev[1] + (zd * h1 + y) * w1 + x;
+            if (a.vec[set] && x + 8 <= w1) {
+                const uint4 u = __ldg(reinterpret_cast<const uint4*>(r0));
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(r0 + p0));
+                lo = __byte_perm(pyr_avg2(u.x, v.x), pyr_avg2(u.y, v.y), 0x6420);
+                hi = __byte_perm(pyr_avg2(u.z, v.z), pyr_avg2(u.w, v.w), 0x6420);
+                if ((w1 & 7) == 0) {
+                    *reinterpret_cast<uint2*>(o) = make_uint2(lo, hi);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) o[k] = (uint8_t)((k < 4 ? lo : hi) >> (8 * (k & 3)));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (x + k < w1) {
+                        const uint8_t* q = r0 + 2 * k;
+                        const uint32_t v = ((uint32_t)q[0] + q[1] + q[p0] + q[p0 + 1] + 2u) >> 2;
+                        o[k] = (uint8_t)v;
+                        if (k < 4) lo |= v << (8 * k); else hi |= v << (8 * (k - 4));
+                    }
+                }
+            }
         }
-        t[0][ty][tx] = v;
+        *reinterpret_cast<uint2*>(&t1[ty][tx]) = make_uint2(lo, hi);
     }
+    // levels >= 2 from the previous level's tile
     for (int L = 2; L < a.nlev; ++L) {
         __syncthreads();
-        const int side = 16 >> (L - 1);
-        if (tx < side && ty < side) {
-            const int x = blockIdx.x * side + tx, y = blockIdx.y * side + ty;
-            const int v = (t[cur][2 * ty][2 * tx] + t[cur][2 * ty][2 * tx + 1] + t[cur][2 * ty + 1][2 * tx] +
-                           t[cur][2 * ty + 1][2 * tx + 1] + 2) >> 2;
-            if (x < a.w[L] && y < a.h[L]) a.lev[L][((long long)z * a.h[L] + y) * a.w[L] + x] = (uint8_t)v;
-            t[cur ^ 1][ty][tx] = v;
+        const int tw = kPyrTX >> (L - 1), th = kPyrTY >> (L - 1);
+        const int wL = a.w[L], hL = a.h[L];
+        for (int k = tid; k < tw * th; k += 256) {
+            const int ty = k / tw, tx = k - ty * tw;
+            uint32_t v;
+            if (L & 1) {   // L = 3, 5: from t2 (level L-1)
+                v = ((uint32_t)t2[2 * ty][2 * tx] + t2[2 * ty][2 * tx + 1] + t2[2 * ty + 1][2 * tx] +
+                     t2[2 * ty + 1][2 * tx + 1] + 2u) >> 2;
+            } else {       // L = 2, 4: from t1
+                v = ((uint32_t)t1[2 * ty][2 * tx] + t1[2 * ty][2 * tx + 1] + t1[2 * ty + 1][2 * tx] +
+                     t1[2 * ty + 1][2 * tx + 1] + 2u) >> 2;
+            }
+            const int x = blockIdx.x * tw + tx, y = blockIdx.y * th + ty;
+            if (x < wL && y < hL) a.lev[L][(zd * hL + y) * wL + x] = (uint8_t)v;
+            if (L & 1) t1[ty][tx] = (uint8_t)v;
+            else t2[ty][tx] = (uint8_t)v;
         }
-        cur ^= 1;
     }
 }
 

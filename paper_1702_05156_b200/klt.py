@@ -9,7 +9,8 @@ from dataclasses import dataclass, fields
 
 from .dmsgm import DMSGM_OK, DmsgmError, _check_tensor, _ptr, _stream_handle, lib
 
-KLT_EXPORTS = ("dmsgm_klt_create", "dmsgm_klt_estimate", "dmsgm_klt_corners", "dmsgm_klt_track",
+KLT_EXPORTS = ("dmsgm_klt_create", "dmsgm_klt_estimate", "dmsgm_klt_estimate_seq", "dmsgm_klt_seq_reset",
+               "dmsgm_klt_corners", "dmsgm_klt_track",
                "dmsgm_klt_ransac", "dmsgm_klt_get_status", "dmsgm_klt_levels",
                "dmsgm_klt_kernels_per_estimate", "dmsgm_klt_last_error", "dmsgm_klt_destroy")
 
@@ -48,6 +49,8 @@ def _setup(L):
     P, i32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
     L.dmsgm_klt_create.argtypes = [i32, i32, ctypes.POINTER(dmsgm_klt_params), i32, ctypes.POINTER(P)]
     L.dmsgm_klt_estimate.argtypes = [P, P, sz, P, sz, P, P, P]
+    L.dmsgm_klt_estimate_seq.argtypes = [P, P, sz, P, sz, P, P, P]
+    L.dmsgm_klt_seq_reset.argtypes = [P]
     L.dmsgm_klt_corners.argtypes = [P, P, sz, P, P, P]
     L.dmsgm_klt_track.argtypes = [P, P, sz, P, sz, P, P, P, P, P]
     L.dmsgm_klt_ransac.argtypes = [P, P, P, P, P, P, P, P, P]
@@ -106,6 +109,22 @@ class Klt:
             _check_tensor("ok_out", ok_out, (S,), "int32", self.device)
         self._check(self._lib.dmsgm_klt_estimate(self._h, _ptr(prev), prev.stride(-2), _ptr(nxt), nxt.stride(-2),
                                                  _ptr(H_out), _ptr(ok_out), _stream_handle(stream)))
+
+    def estimate_seq(self, prev, nxt, H_out, ok_out=None, stream=None):
+        """estimate() for consecutive pairs of a video: reuses the corners and pyramid of `prev`
+        when it is the buffer passed as `nxt` to the previous call (its content unchanged --
+        the caller's guarantee; seq_reset() otherwise), include/dmsgm_klt.h."""
+        S = self.params.num_streams
+        self._frames("prev", prev)
+        self._frames("next", nxt)
+        _check_tensor("H_out", H_out, (S, 9), "float64", self.device)
+        if ok_out is not None:
+            _check_tensor("ok_out", ok_out, (S,), "int32", self.device)
+        self._check(self._lib.dmsgm_klt_estimate_seq(self._h, _ptr(prev), prev.stride(-2), _ptr(nxt), nxt.stride(-2),
+                                                     _ptr(H_out), _ptr(ok_out), _stream_handle(stream)))
+
+    def seq_reset(self):
+        self._check(self._lib.dmsgm_klt_seq_reset(self._h))
 
     def corners(self, frames, corners_out, counts_out, stream=None):
         S, M = self.params.num_streams, self.params.max_corners

@@ -28,5 +28,16 @@ for i in range(reps):
 e1.record(st)
 e1.synchronize()
 ms = e0.elapsed_time(e1) / reps
+# consecutive pairs through dmsgm_klt_estimate_seq (frames 0..7 of the ring, then 7 -> 0: a
+# continuous motion, the ring is periodic)
+for i in range(3):
+    k.estimate_seq(frames[i % 8], frames[(i + 1) % 8], He, ok)
+e0.record(st)
+for i in range(3, 3 + reps):
+    k.estimate_seq(frames[i % 8], frames[(i + 1) % 8], He, ok)
+e1.record(st)
+e1.synchronize()
+ms_seq = e0.elapsed_time(e1) / reps
 print(json.dumps({"config": name, "streams": S, "ms_per_estimate": ms, "frames_per_s": S / (ms / 1e3),
+                  "ms_per_estimate_seq": ms_seq, "frames_per_s_seq": S / (ms_seq / 1e3),
                   "inliers_min": int(ok.min()), "status": k.get_status(), "levels": k.levels}))
