@@ -178,6 +178,10 @@ cudaError_t launch_track(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, c
     const dim3 grid((c->p.max_corners + 7) / 8, c->S);
     const int ns = (c->p.win * c->p.win + 31) / 32;
     if (ns <= 8) klt_lk_kernel<8><<<grid, 256, 0, st>>>(la);
+#ifndef DMSGM_LK_WIN20
+#define DMSGM_LK_WIN20 1
+#endif
+    else if (DMSGM_LK_WIN20 && c->p.win == 20) klt_lk_kernel<13, 20><<<grid, 256, 0, st>>>(la);   // App. F's Size(20,20)
     else if (ns <= 13) klt_lk_kernel<13><<<grid, 256, 0, st>>>(la);
     else klt_lk_kernel<32><<<grid, 256, 0, st>>>(la);
     return cudaGetLastError();

@@ -676,14 +676,21 @@ constexpr int kLkWarps = 8;
 constexpr int kLkMaxWin = 32;
 
 #ifndef DMSGM_LK_MINB
-#define DMSGM_LK_MINB 3
+#define DMSGM_LK_MINB 2
 #endif
 #ifndef DMSGM_LK_PAIRED
 #define DMSGM_LK_PAIRED 1
 #endif
-constexpr int kLkMargin = 4;     // next-image region: the window +- this many pixels of flow per level
+constexpr int kLkMargin = 4;
+#ifndef DMSGM_LK_BATCH
+#define DMSGM_LK_BATCH 8
+#endif
+constexpr int kLkBatch = DMSGM_LK_BATCH;   // staging rows per batch of loads     // next-image region: the window +- this many pixels of flow per level
 
-template <int NS>   // samples per lane: ceil(win^2 / 32)
+// NS = samples per lane: ceil(win^2 / 32); WIN = the window as a compile-time constant (the
+// paper's Size(20,20): every window-geometry term folds, the staging loops unroll and the
+// sample offsets are rematerialised for free instead of spilled) or 0 (a.win at run time)
+template <int NS, int WIN = 0>
 __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) klt_lk_kernel(const LkArgs a) {
     constexpr int MW = NS <= 8 ? 16 : (NS <= 13 ? 20 : kLkMaxWin);   // largest window of this variant
     constexpr bool STAGE = NS <= 13;       // (win > 20: the regions would exceed 48 KB; global reads)
@@ -706,7 +713,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
     float* patch = patch_all[threadIdx.x >> 5];
     float* region = region_all[threadIdx.x >> 5];
     const float cx = (float)a.corners[2 * o] + 0.5f, cy = (float)a.corners[2 * o + 1] + 0.5f;
-    const int win = a.win, nsamp = win * win, pw = win + 2, rs = win + 1 + 2 * kLkMargin;
+    const int win = WIN ? WIN : a.win, nsamp = win * win, pw = win + 2, rs = win + 1 + 2 * kLkMargin;
     const float half = 0.5f * (float)(win - 1);
     // sample q = lane + 32 k of the window, (ii, jj) = (q % win, q / win): its offset in the
     // next-image region
@@ -744,11 +751,24 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
                     // row y's horizontal blend is row y+1's top: computed once per image row
                     const uint8_t* r0 = pp + (long long)clampi(Y0 - 1, 0, P.h - 1) * P.pitch;
                     float top = __fadd_rn(__fmul_rn((float)__ldg(r0 + xa), gxw), __fmul_rn((float)__ldg(r0 + xb), fx));
-                    for (int rj = 0; rj < pw; ++rj) {
-                        const uint8_t* rb = pp + (long long)clampi(Y0 + rj, 0, P.h - 1) * P.pitch;
-                        const float bot = __fadd_rn(__fmul_rn((float)__ldg(rb + xa), gxw), __fmul_rn((float)__ldg(rb + xb), fx));
-                        patch[rj * pw + ci] = __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy));
-                        top = bot;
+                    // rows in batches of kLkBatch: the batch's byte loads are all in flight before
+                    // the first blend (one load round trip per batch, not per row)
+                    for (int rj0 = 0; rj0 < pw; rj0 += kLkBatch) {
+                        uint32_t va[kLkBatch], vb[kLkBatch];
+#pragma unroll
+                        for (int u = 0; u < kLkBatch; ++u) {
+                            const uint8_t* rb = pp + (long long)clampi(Y0 + rj0 + u, 0, P.h - 1) * P.pitch;
+                            va[u] = __ldg(rb + xa);
+                            vb[u] = __ldg(rb + xb);
+                        }
+#pragma unroll
+                        for (int u = 0; u < kLkBatch; ++u) {
+                            if (rj0 + u < pw) {
+                                const float bot = __fadd_rn(__fmul_rn((float)va[u], gxw), __fmul_rn((float)vb[u], fx));
+                                patch[(rj0 + u) * pw + ci] = __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy));
+                                top = bot;
+                            }
+                        }
                     }
                 }
             }
@@ -769,9 +789,15 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
                     const int ci = c0 + lane;
                     if (ci < rs) {
                         const int xa = clampi(RX0 + ci, 0, Q.w - 1);
-                        for (int rj = 0; rj < rs; ++rj)
-                            region[rj * rs + ci] =
-                                (float)__ldg(qp + (long long)clampi(RY0 + rj, 0, Q.h - 1) * Q.pitch + xa);
+                        for (int rj0 = 0; rj0 < rs; rj0 += kLkBatch) {
+                            uint32_t v[kLkBatch];
+#pragma unroll
+                            for (int u = 0; u < kLkBatch; ++u)
+                                v[u] = __ldg(qp + (long long)clampi(RY0 + rj0 + u, 0, Q.h - 1) * Q.pitch + xa);
+#pragma unroll
+                            for (int u = 0; u < kLkBatch; ++u)
+                                if (rj0 + u < rs) region[(rj0 + u) * rs + ci] = (float)v[u];
+                        }
                     }
                 }
             }
