@@ -375,18 +375,21 @@ int dmsgm_klt_estimate_seq(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch,
         const int ds[2] = {pset, nset};
         e = launch_corners(c, prev, ppitch, slot_corners(c, pslot), slot_counts(c, pslot), st);
         if (e == cudaSuccess) e = launch_pyramid(c, 2, img, pit, ds, st);
-    } else {
+    }
+    // the corners of next (the next call's prev) on the side stream, beside the pyramid, LK
+    // and the fit of this pair (it waits only for the work already on `cuda_stream`: the
+    // previous call read corner slot nslot there); joined at the end, so the call's work is
+    // complete when `cuda_stream` is
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    if (e == cudaSuccess) e = launch_corners(c, next, npitch, slot_corners(c, nslot), slot_counts(c, nslot), c->side);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_pyr, c->side);
+    if (e == cudaSuccess && cached) {
         const uint8_t* img[1] = {next};
         const size_t pit[1] = {npitch};
         const int ds[1] = {nset};
         e = launch_pyramid(c, 1, img, pit, ds, st);
     }
-    // the corners of next (the next call's prev) on the side stream, beside LK and the fit of
-    // this pair; joined at the end, so the call's work is complete when `cuda_stream` is
-    if (e == cudaSuccess) e = cudaEventRecord(c->ev_fork, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
-    if (e == cudaSuccess) e = launch_corners(c, next, npitch, slot_corners(c, nslot), slot_counts(c, nslot), c->side);
-    if (e == cudaSuccess) e = cudaEventRecord(c->ev_pyr, c->side);
     if (e == cudaSuccess)
         e = launch_track(c, prev, ppitch, next, npitch, slot_corners(c, pslot), slot_counts(c, pslot), c->tracked,
                          c->status, st, true, pset, nset);

@@ -151,7 +151,10 @@ __global__ void __launch_bounds__(256) klt_score_kernel(const ScoreArgs a) {
 // ring.  Candidates and the per-stream maximum exactly as K1.  ~8x fewer instructions than K1,
 // whose 32x8 tiles recompute 1.7x the gradients and 1.3x the scores with byte loads.
 constexpr int kScoreBand = 120;
-constexpr int kScorePrefetch = 8;
+#ifndef DMSGM_SCORE_PREFETCH
+#define DMSGM_SCORE_PREFETCH 8
+#endif
+constexpr int kScorePrefetch = DMSGM_SCORE_PREFETCH;
 constexpr int kCbuf = 384;          // per-warp candidate buffer (keys): flushed above kCbuf - 128
 constexpr int kScoreWarps = 8;
 
@@ -200,6 +203,9 @@ __global__ void __launch_bounds__(32 * kScoreWarps) klt_score_stream_kernel(cons
         nbuf = 0;
     };
     const int r0 = ys - 3, r1 = ye + 2;
+    // the input word of the NEXT row is loaded one row ahead (its L1 / L2 latency hides
+    // behind this row's arithmetic)
+    uint32_t wnext = __ldg(reinterpret_cast<const unsigned int*>(f + (long long)clampi(r0, 0, H - 1) * a.pitch + off));
     for (int rb = r0; rb <= r1; rb += 3) {
 #pragma unroll
         for (int ph = 0; ph < 3; ++ph) {
@@ -207,10 +213,10 @@ __global__ void __launch_bounds__(32 * kScoreWarps) klt_score_stream_kernel(cons
             if (r > r1) break;                             // warp-uniform
             // --- input row r: dX, sX of columns x .. x+3 ---
             {
-                const uint8_t* row = f + (long long)clampi(r, 0, H - 1) * a.pitch;
-                // the row kScorePrefetch ahead into L1: this row's load then waits ~L1, not HBM
+                // the row kScorePrefetch ahead into L1: the one-ahead load then waits ~L1, not HBM
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(f + (long long)clampi(r + kScorePrefetch, 0, H - 1) * a.pitch + off));
-                const uint32_t w = __byte_perm(__ldg(reinterpret_cast<const unsigned int*>(row + off)), 0u, sel);
+                const uint32_t w = __byte_perm(wnext, 0u, sel);
+                wnext = __ldg(reinterpret_cast<const unsigned int*>(f + (long long)clampi(r + 1, 0, H - 1) * a.pitch + off));
                 const uint32_t wl = __shfl_up_sync(0xffffffffu, w, 1), wr = __shfl_down_sync(0xffffffffu, w, 1);
                 int p[6];
                 p[0] = (int)(wl >> 24);
