@@ -834,6 +834,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
                                     0.5f);
         const float det = __fsub_rn(__fmul_rn(gxx, gyy), __fmul_rn(gxy, gxy));
         float vx = 0.0f, vy = 0.0f;
+        const float rdet = __frcp_rn(det);
         if (__fdiv_rn(lam, (float)nsamp) < a.min_eig || !(det > 0.0f)) {
             if (L == 0) { ok = false; break; }
             gx = __fmul_rn(2.0f, gx);                    // a coarse level without texture: skipped
@@ -914,8 +915,10 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
             }
             bx = warp_sum(bx);
             by = warp_sum(by);
-            const float dx = __fdiv_rn(__fsub_rn(__fmul_rn(gyy, bx), __fmul_rn(gxy, by)), det);
-            const float dy = __fdiv_rn(__fsub_rn(__fmul_rn(gxx, by), __fmul_rn(gxy, bx)), det);
+            // G^-1 b with the level's 1/det (one correctly rounded reciprocal per level instead
+            // of two IEEE divisions per iteration; LK is compared within a tolerance, R40)
+            const float dx = __fmul_rn(__fsub_rn(__fmul_rn(gyy, bx), __fmul_rn(gxy, by)), rdet);
+            const float dy = __fmul_rn(__fsub_rn(__fmul_rn(gxx, by), __fmul_rn(gxy, bx)), rdet);
             vx = __fadd_rn(vx, dx);
             vy = __fadd_rn(vy, dy);
             if (L == 0) {
