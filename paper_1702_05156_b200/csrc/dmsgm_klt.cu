@@ -175,15 +175,15 @@ cudaError_t launch_track(dmsgm_klt_ctx* c, const uint8_t* prev, size_t ppitch, c
     la.nlev = c->nlev; la.win = c->p.win; la.max_iters = c->p.max_iters; la.max_corners = c->p.max_corners;
     la.eps2 = c->p.eps * c->p.eps; la.min_eig = c->p.min_eig;
     la.corners = corners; la.counts = counts; la.tracked = tracked; la.status = status;
-    const dim3 grid((c->p.max_corners + 7) / 8, c->S);
+    const dim3 grid((c->p.max_corners + kLkWarps - 1) / kLkWarps, c->S);
     const int ns = (c->p.win * c->p.win + 31) / 32;
-    if (ns <= 8) klt_lk_kernel<8><<<grid, 256, 0, st>>>(la);
+    if (ns <= 8) klt_lk_kernel<8><<<grid, 32 * kLkWarps, 0, st>>>(la);
 #ifndef DMSGM_LK_WIN20
 #define DMSGM_LK_WIN20 1
 #endif
-    else if (DMSGM_LK_WIN20 && c->p.win == 20) klt_lk_kernel<13, 20><<<grid, 256, 0, st>>>(la);   // App. F's Size(20,20)
-    else if (ns <= 13) klt_lk_kernel<13><<<grid, 256, 0, st>>>(la);
-    else klt_lk_kernel<32><<<grid, 256, 0, st>>>(la);
+    else if (DMSGM_LK_WIN20 && c->p.win == 20) klt_lk_kernel<13, 20><<<grid, 32 * kLkWarps, 0, st>>>(la);   // App. F's Size(20,20)
+    else if (ns <= 13) klt_lk_kernel<13><<<grid, 32 * kLkWarps, 0, st>>>(la);
+    else klt_lk_kernel<32><<<grid, 32 * kLkWarps, 0, st>>>(la);
     return cudaGetLastError();
 }
 

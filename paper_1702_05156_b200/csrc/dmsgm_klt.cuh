@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArg
     uint16_t* grid_s = reinterpret_cast<uint16_t*>(pcell + kBatch);
     __shared__ unsigned long long s_prefix, s_mask;
     __shared__ unsigned s_rem, s_total, s_m;
-    __shared__ int s_nkept, s_done;
+    __shared__ int s_nkept, s_done, s_exact;
     const int s = blockIdx.x, tid = threadIdx.x;
     const unsigned cnt = a.count[s];
     if (tid == 0 && cnt > (unsigned)a.cap) *a.overflow = 1u;
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArg
     unsigned long long upper = ~0ull;             // this batch: keys below `upper`
     while (!s_done) {
         // ---- exact radix select of the kBatch-th largest qualifying key below `upper` ----
-        if (tid == 0) { s_prefix = 0; s_mask = 0; s_rem = kBatch; }
+        if (tid == 0) { s_prefix = 0; s_mask = 0; s_rem = kBatch; s_exact = 0; }
         unsigned long long cut = 0;
         bool all = false;
         for (int pass = 0; pass < 8; ++pass) {
@@ -412,10 +412,15 @@ __global__ void __launch_bounds__(kSelThreads) klt_select_kernel(const SelectArg
                     s_rem = rem - cum;
                     s_prefix |= (unsigned long long)d << shift;
                     s_mask |= 0xFFull << shift;
+                    // the whole bucket d is needed: keys >= prefix | d << shift (low bits 0)
+                    // are exactly the kBatch largest -- the remaining passes would only find
+                    // the smallest of them
+                    s_exact = hist[d] == rem - cum;
                 }
             }
             __syncthreads();
             if (s_total <= (unsigned)kBatch) { all = true; break; }
+            if (s_exact) break;
         }
         if (!all) cut = s_prefix;                 // the kBatch-th largest key (keys are unique)
         // ---- gather the batch: qualifying keys in [cut, upper) ----
@@ -678,31 +683,32 @@ __device__ __forceinline__ float pix_clamped(const uint8_t* img, int pitch, int 
 // On next, each iteration's samples s + g + v likewise share one fractional offset (the
 // guess is added to the window's base point once), so a sample is 4 byte loads and the
 // blend with common weights; windows wholly inside the level image skip the clamps.
-constexpr int kLkWarps = 8;
+constexpr int kLkWarps = 4;       // warps (corners) per CTA
 constexpr int kLkMaxWin = 32;
 
 #ifndef DMSGM_LK_MINB
-#define DMSGM_LK_MINB 2
+#define DMSGM_LK_MINB 4
 #endif
 #ifndef DMSGM_LK_PAIRED
 #define DMSGM_LK_PAIRED 1
 #endif
-constexpr int kLkMargin = 4;
+constexpr int kLkMargin = 4;     // next-image region: the window +- this many pixels of flow per level
 #ifndef DMSGM_LK_BATCH
 #define DMSGM_LK_BATCH 8
 #endif
-constexpr int kLkBatch = DMSGM_LK_BATCH;   // staging rows per batch of loads     // next-image region: the window +- this many pixels of flow per level
+constexpr int kLkBatch = DMSGM_LK_BATCH;   // staging rows per batch of loads
 
 // NS = samples per lane: ceil(win^2 / 32); WIN = the window as a compile-time constant (the
-// paper's Size(20,20): every window-geometry term folds, the staging loops unroll and the
-// sample offsets are rematerialised for free instead of spilled) or 0 (a.win at run time)
+// paper's Size(20,20): the window-geometry terms fold) or 0 (a.win at run time).  The staged
+// next-image region holds (pixel, right neighbour) pairs, so a sample's 4 taps are two
+// 8-byte shared loads.
 template <int NS, int WIN = 0>
 __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) klt_lk_kernel(const LkArgs a) {
     constexpr int MW = NS <= 8 ? 16 : (NS <= 13 ? 20 : kLkMaxWin);   // largest window of this variant
     constexpr bool STAGE = NS <= 13;       // (win > 20: the regions would exceed 48 KB; global reads)
     constexpr int MR = STAGE ? MW + 1 + 2 * kLkMargin : 1;             // next-region side
     __shared__ float patch_all[kLkWarps][(MW + 2) * (MW + 2)];
-    __shared__ float region_all[kLkWarps][MR * MR];
+    __shared__ float2 region_all[kLkWarps][MR * MR];   // (v[y][x], v[y][x+1])
     const int lane = threadIdx.x & 31;
     const int i = blockIdx.x * kLkWarps + (threadIdx.x >> 5);
     const int s = blockIdx.y;
@@ -717,7 +723,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
         return;
     }
     float* patch = patch_all[threadIdx.x >> 5];
-    float* region = region_all[threadIdx.x >> 5];
+    float2* region = region_all[threadIdx.x >> 5];
     const float cx = (float)a.corners[2 * o] + 0.5f, cy = (float)a.corners[2 * o + 1] + 0.5f;
     const int win = WIN ? WIN : a.win, nsamp = win * win, pw = win + 2, rs = win + 1 + 2 * kLkMargin;
     const float half = 0.5f * (float)(win - 1);
@@ -794,15 +800,18 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
                 for (int c0 = 0; c0 < rs; c0 += 32) {
                     const int ci = c0 + lane;
                     if (ci < rs) {
-                        const int xa = clampi(RX0 + ci, 0, Q.w - 1);
+                        const int xa = clampi(RX0 + ci, 0, Q.w - 1), xb = clampi(RX0 + ci + 1, 0, Q.w - 1);
                         for (int rj0 = 0; rj0 < rs; rj0 += kLkBatch) {
-                            uint32_t v[kLkBatch];
+                            uint32_t v[kLkBatch], w[kLkBatch];
+#pragma unroll
+                            for (int u = 0; u < kLkBatch; ++u) {
+                                const uint8_t* row = qp + (long long)clampi(RY0 + rj0 + u, 0, Q.h - 1) * Q.pitch;
+                                v[u] = __ldg(row + xa);
+                                w[u] = __ldg(row + xb);
+                            }
 #pragma unroll
                             for (int u = 0; u < kLkBatch; ++u)
-                                v[u] = __ldg(qp + (long long)clampi(RY0 + rj0 + u, 0, Q.h - 1) * Q.pitch + xa);
-#pragma unroll
-                            for (int u = 0; u < kLkBatch; ++u)
-                                if (rj0 + u < rs) region[(rj0 + u) * rs + ci] = (float)v[u];
+                                if (rj0 + u < rs) region[(rj0 + u) * rs + ci] = make_float2((float)v[u], (float)w[u]);
                         }
                     }
                 }
@@ -856,7 +865,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
                 // the window (and its +1 neighbours) inside the staged region; branch-free: a
                 // lane's padding samples (q >= win^2) read offset 0 and have I = Ix = Iy = 0, so
                 // they add exactly +0 to both sums
-                const float* base = region + dyr * rs + dxr;
+                const float2* base = region + dyr * rs + dxr;
 #if DMSGM_LK_PAIRED
                 // two samples per paired instruction (FFMA2 / FMUL2 / FADD2), the blend and
                 // the sums as fmas: ~4.5 FP instructions per sample instead of 12 (LK is
@@ -865,10 +874,11 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
                 float2 bx2 = f2_bc(0.0f), by2 = f2_bc(0.0f);
 #pragma unroll
                 for (int k = 0; k + 1 < NS; k += 2) {
-                    const float* ra = base + roff[k];
-                    const float* rb = base + roff[k + 1];
-                    const float2 p00 = make_float2(ra[0], rb[0]), p10 = make_float2(ra[1], rb[1]);
-                    const float2 p01 = make_float2(ra[rs], rb[rs]), p11 = make_float2(ra[rs + 1], rb[rs + 1]);
+                    const float2* ra = base + roff[k];
+                    const float2* rb = base + roff[k + 1];
+                    const float2 ta = ra[0], tb = rb[0], ua = ra[rs], ub = rb[rs];   // (left, right) taps
+                    const float2 p00 = make_float2(ta.x, tb.x), p10 = make_float2(ta.y, tb.y);
+                    const float2 p01 = make_float2(ua.x, ub.x), p11 = make_float2(ua.y, ub.y);
                     const float2 top = f2_fma(p00, GXW, f2_mul(p10, FX));
                     const float2 bot = f2_fma(p01, GXW, f2_mul(p11, FX));
                     const float2 e = f2_sub(make_float2(I[k], I[k + 1]), f2_fma(top, GYW, f2_mul(bot, FY)));
@@ -878,9 +888,10 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
                 bx = __fadd_rn(bx2.x, bx2.y);
                 by = __fadd_rn(by2.x, by2.y);
                 if constexpr (NS & 1) {
-                    const float* r0 = base + roff[NS - 1];
-                    const float top = __fmaf_rn(r0[0], gxw, __fmul_rn(r0[1], fx));
-                    const float bot = __fmaf_rn(r0[rs], gxw, __fmul_rn(r0[rs + 1], fx));
+                    const float2* r0 = base + roff[NS - 1];
+                    const float2 t0 = r0[0], u0 = r0[rs];
+                    const float top = __fmaf_rn(t0.x, gxw, __fmul_rn(t0.y, fx));
+                    const float bot = __fmaf_rn(u0.x, gxw, __fmul_rn(u0.y, fx));
                     const float e = __fsub_rn(I[NS - 1], __fmaf_rn(top, gyw, __fmul_rn(bot, fy)));
                     bx = __fmaf_rn(e, Ix[NS - 1], bx);
                     by = __fmaf_rn(e, Iy[NS - 1], by);
@@ -888,8 +899,8 @@ __global__ void __launch_bounds__(32 * kLkWarps, NS <= 13 ? DMSGM_LK_MINB : 1) k
 #else
 #pragma unroll
                 for (int k = 0; k < NS; ++k) {
-                    const float* r0 = base + roff[k];
-                    const float p00 = r0[0], p10 = r0[1], p01 = r0[rs], p11 = r0[rs + 1];
+                    const float2* r0 = base + roff[k];
+                    const float p00 = r0[0].x, p10 = r0[0].y, p01 = r0[rs].x, p11 = r0[rs].y;
                     const float top = __fadd_rn(__fmul_rn(p00, gxw), __fmul_rn(p10, fx));
                     const float bot = __fadd_rn(__fmul_rn(p01, gxw), __fmul_rn(p11, fx));
                     const float e = __fsub_rn(I[k], __fadd_rn(__fmul_rn(top, gyw), __fmul_rn(bot, fy)));
