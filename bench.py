@@ -255,6 +255,24 @@ def cores_available():
 
 
 # ---------------------------------------------------------------------------
+def arm_config(args, world, W, H, N, S, total_streams, bytes_per_step, slot_bytes, pf=None):
+    """The bench line's `config`.  The reference arm reports the same object: it times a bounded
+    sample of this workload on the host (the sample is stated in its cpu_baseline)."""
+    wl = WORKLOADS[args.config]
+    return {"workload": args.config + ("+prefilter" if pf else "") +
+                        {"frame": "+framewarp", "estimate": "+klt"}.get(args.motion, "") +
+                        ("+bitmasks" if args.masks == "bits" else ""),
+            "mask_format": args.masks,
+            "desc": wl["desc"], "W": W, "H": H, "motion_compensation": args.motion,
+            "N": N, "prefilter": {"gauss_size": pf[0], "gauss_sigma": pf[1], "median_radius": pf[2]}
+            if pf else None,
+            "streams_per_gpu": S, "total_streams": total_streams, "ring_frames": RING,
+            "l2": f"inputs larger than L2: {bytes_per_step / 1e6:.1f} MB algorithmic traffic per step; "
+                  f"{GRAPH_T} frame + mask slots per stream ({RING} distinct frames repeated), "
+                  f"{slot_bytes / 1e9:.2f} GB",
+            "parallelism": f"stream-sharded x{world}, no data-path collective"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle as it stands on this box's host cores, same config."""
     if rank != 0:
@@ -297,13 +315,19 @@ def run_reference(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, "desc": wl["desc"], "W": cfg.W, "H": cfg.H, "N": cfg.N,
-                   "streams_per_step": ns},
+        # the arm's own config (the plain step: the reference arm runs no prefilter / warp /
+        # estimation; the per-step bytes are the library's algorithmic count for it:
+        # frame + mask + 2 x 24-byte block records per block)
+        "config": arm_config(args, world, cfg.W, cfg.H, cfg.N, cfg.S,
+                             world * cfg.S if args.scaling == "weak" else cfg.S,
+                             cfg.S * (2.0 * cfg.W * cfg.H + 48.0 * -(-cfg.W // cfg.N) * -(-cfg.H // cfg.N)),
+                             2 * GRAPH_T * cfg.S * cfg.H * cfg.W),
         "mpixel_per_s": fps * cfg.W * cfg.H / 1e6,
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": min(cores, ns), "kind": "oracle",
                          "cpu_model": cpu_model(),
-                         "sample": f"{ns} streams x 1 frame per step, {args.steps} timed steps, plain C oracle "
-                                   f"(-O2, single-threaded per stream, one thread per stream)"},
+                         "sample": f"{ns} of the {cfg.S} streams x 1 frame per step, {args.steps} timed steps, "
+                                   f"plain C oracle (-O2, single-threaded per stream, one thread per stream)",
+                         "streams_per_step": ns},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -596,18 +620,8 @@ def run_dmsgm(args, rank, world, local):
                       f"median_ms_per_step = median over the {len(rep_ms)} full replays",
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth/ ring recipe, generated on device)",
-            "config": {"workload": args.config + ("+prefilter" if pf else "") +
-                                   {"frame": "+framewarp", "estimate": "+klt"}.get(args.motion, "") +
-                                   ("+bitmasks" if args.masks == "bits" else ""),
-                       "mask_format": args.masks,
-                       "desc": wl["desc"], "W": W, "H": H, "motion_compensation": args.motion,
-                       "N": N, "prefilter": {"gauss_size": pf[0], "gauss_sigma": pf[1], "median_radius": pf[2]}
-                       if pf else None,
-                       "streams_per_gpu": S, "total_streams": total_streams, "ring_frames": RING,
-                       "l2": f"inputs larger than L2: {bytes_per_step / 1e6:.1f} MB algorithmic traffic per step; "
-                             f"{GRAPH_T} frame + mask slots per stream ({RING} distinct frames repeated), "
-                             f"{(frames.numel() + masks.numel()) / 1e9:.2f} GB",
-                       "parallelism": f"stream-sharded x{world}, no data-path collective"},
+            "config": arm_config(args, world, W, H, N, S, total_streams, bytes_per_step,
+                                 frames.numel() + masks.numel(), pf),
             "mpixel_per_s": fps * W * H / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "spec_peak": SPEC_HBM_GBS, "frac_of_spec": achieved / SPEC_HBM_GBS,

@@ -22,6 +22,10 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["config"]["workload"] == "C4"
+    # the same config object as the GPU arm's line (profiles/R2f_bench_C4.json, same defaults)
+    with open(os.path.join(ROOT, "profiles", "R2f_bench_C4.json")) as f:
+        assert line["config"] == json.loads(f.read())["config"]
+    assert 1 <= line["cpu_baseline"]["streams_per_step"] <= line["config"]["streams_per_gpu"]
 
 
 def test_warmup_bound():
