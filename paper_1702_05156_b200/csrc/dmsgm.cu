@@ -462,7 +462,7 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
                  : launch_staged<NN, BB, 3, false, true>(c, a, frames, fpitch, s0, count, parity, slot, stream,  \
                                                          early_frames)
         if (c->band) {   // band mode: halo check + neighbour stores compiled in
-            if (c->N == 1) { DMSGM_BAND(1, 2); }
+            if (c->N == 1) { DMSGM_BAND(1, DMSGM_N1_BPT); }
             if (c->N == 2) { DMSGM_BAND(2, 2); }
             if (c->N == 4) { DMSGM_BAND(4, 2); }
             DMSGM_BAND(8, 1);
@@ -482,7 +482,7 @@ cudaError_t launch_step(dmsgm_ctx* c, const uint8_t* frames, size_t fpitch, cons
     if (c->mask_bits) { DMSGM_STAGED_BITS(NN, BB); }  \
     if (c->staged_occ == 3) { DMSGM_STAGED(NN, BB, 3); } \
     DMSGM_STAGED(NN, BB, 4)
-        if (c->N == 1) { DMSGM_STAGED(1, 2, 3); }
+        if (c->N == 1) { DMSGM_STAGED(1, DMSGM_N1_BPT, 3); }
         if (c->N == 2) { DMSGM_STAGED(2, 2, 3); }
         if (c->N == 4) { DMSGM_STAGED_OCC(4, 2); }
         if (c->N == 8) { DMSGM_STAGED_OCC(8, 1); }
@@ -615,7 +615,7 @@ int dmsgm_create(int width, int height, int block, const dmsgm_params* p, int de
             c->pdl = !(penv && atoi(penv) == 0);
 #define DMSGM_SETUP(NN, BB) (c->staged_occ == 3 ? setup_staged<NN, BB, 3>(c) : setup_staged<NN, BB, 4>(c))
             if (block < 4) c->staged_occ = 3;   // (the 4-CTA variants exist for N = 4 and 8 only)
-            e = block == 1 ? setup_staged<1, 2, 3>(c)
+            e = block == 1 ? setup_staged<1, DMSGM_N1_BPT, 3>(c)
               : block == 2 ? setup_staged<2, 2, 3>(c)
               : block == 4 ? DMSGM_SETUP(4, 2) : DMSGM_SETUP(8, 1);
 #undef DMSGM_SETUP
@@ -930,12 +930,12 @@ int dmsgm_get_info(const dmsgm_ctx* c, dmsgm_info* out) {
     if (c->wf_buf) out->algorithmic_bytes_per_frame += 2.0 * c->W * c->Hp;     // frame warp: read + write
     if (c->staged)
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,%d%s> (TMA, persistent)", c->N,
-                 c->N == 8 ? 1 : 2, c->staged_occ, c->mask_bits ? ",bits" : "");
+                 c->N == 8 ? 1 : (c->N == 1 ? DMSGM_N1_BPT : 2), c->staged_occ, c->mask_bits ? ",bits" : "");
     else
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_kernel<%d,%d>", c->N, bpt_of(c));
     if (c->staged && c->band)
         snprintf(out->kernel, sizeof out->kernel, "dmsgm_step_staged<%d,%d,3,band> (TMA, persistent)",
-                 c->N, c->N == 8 ? 1 : 2);
+                 c->N, c->N == 8 ? 1 : (c->N == 1 ? DMSGM_N1_BPT : 2));
     return DMSGM_OK;
 }
 
