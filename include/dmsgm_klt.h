@@ -44,7 +44,7 @@ extern "C" {
 #endif
 
 typedef struct {
-    int    num_streams;    /* S >= 1                                                           */
+    int    num_streams;    /* 1 <= S <= 32767                                                   */
     int    max_corners;    /* goodFeaturesToTrack maxCorners, 4..1024                           */
     double quality;        /* qualityLevel in (0, 1]                                            */
     double min_distance;   /* minDistance >= 1 (px)                                             */

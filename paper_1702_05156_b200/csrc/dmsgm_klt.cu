@@ -86,7 +86,8 @@ struct Dev {
 
 bool params_ok(const dmsgm_klt_params* p, char* why, size_t n) {
     if (!p) { snprintf(why, n, "params is NULL"); return false; }
-    if (p->num_streams < 1 || p->num_streams > 65535) { snprintf(why, n, "num_streams must be in [1, 65535]"); return false; }
+    // (the pyramid kernel covers two images of every stream in one grid dimension: 2 S <= 65535)
+    if (p->num_streams < 1 || p->num_streams > 32767) { snprintf(why, n, "num_streams must be in [1, 32767]"); return false; }
     if (p->max_corners < 4 || p->max_corners > kMaxCorners) { snprintf(why, n, "max_corners must be in [4, %d]", kMaxCorners); return false; }
     if (!(p->quality > 0.0 && p->quality <= 1.0)) { snprintf(why, n, "quality must be in (0, 1]"); return false; }
     if (!(p->min_distance >= 1.0 && p->min_distance <= 4096.0)) { snprintf(why, n, "min_distance must be in [1, 4096]"); return false; }
