@@ -36,7 +36,7 @@ if ROOT not in sys.path:
 L2_BYTES = 126 * 1024 * 1024
 RING = 8          # distinct synthetic frames per stream (periodic camera motion, no seam)
 GRAPH_T = 40      # steps per CUDA-graph replay (dmsgm_step_n) in the timed region
-PRESLEEP_CYCLES = 200_000   # ~100 us spin kernel queued before the start event (host launch latency)
+PRESLEEP_CYCLES = 2_000_000  # ~1 ms spin kernel queued before the start event (host launch latency)
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 SPEC_HBM_GBS = 8000.0       # B200 datasheet HBM3e bandwidth: BASELINE.md §3's denominator, reported beside
 
@@ -452,6 +452,7 @@ def run_dmsgm(args, rank, world, local):
         # `value` stays the K-step region's)
         T0 = chunks[0]
         mev = [torch.cuda.Event(enable_timing=True) for _ in range(11)]
+        torch.cuda._sleep(PRESLEEP_CYCLES)              # (the same launch-latency cover as the region)
         mev[0].record(stream)
         for k in range(10):
             replay(T0)
@@ -627,7 +628,7 @@ def run_dmsgm(args, rank, world, local):
             "timing": f"{len(chunks)} " + ("CUDA-graph replays of dmsgm_step_n" if args.launch == "graph" else
                                            "groups of single dmsgm_step launches") + f" ({GRAPH_T} steps each"
                       f"{'' if args.steps % GRAPH_T == 0 else ', the last ' + str(args.steps % GRAPH_T)}) "
-                      f"between CUDA events on the launching stream (a ~100 us spin kernel queued ahead of the start "
+                      f"between CUDA events on the launching stream (a ~1 ms spin kernel queued ahead of the start "
                       f"event hides the host's launch latency); value from the whole K-step region, "
                       f"median_ms_per_step = median over {len(rep_ms)} replays (the region's full {GRAPH_T}-step "
                       f"replays, or with fewer than 10 of them 10 replays of its first graph after the region)",
