@@ -95,3 +95,56 @@ def test_ragged_frames_match_oracle(cuda_lib, crop, pad):
             e = _corner_err(Hg[s].cpu().numpy(), Ho, W, H)
             assert e < 0.1, (t, s, e)
     k.close()
+
+
+def test_outputs_stay_in_bounds(cuda_lib):
+    """No KLT entry point writes past its outputs (the pool's compute-sanitizer is closed, see
+    tests/test_gpu_sanitizer.py): every output is a view into a larger buffer filled with a
+    canary byte; after corners / track / ransac / estimate / estimate_seq on ragged frames the
+    bytes around each view are unchanged."""
+    import torch
+    dm = cuda_lib
+    S = 2
+    host, f = _frames("C2", 3, S, (310, 230), 11)
+    H, W = host.shape[2:]
+    kp = dm.KltParams(num_streams=S)
+    M = kp.max_corners
+    k = dm.Klt(W, H, kp)
+    CAN = 0xA5
+
+    def guarded(shape, dtype):
+        n = int(np.prod(shape)) * torch.tensor([], dtype=dtype).element_size()
+        raw = torch.full((n + 2048,), CAN, dtype=torch.uint8, device="cuda")
+        return raw, raw[1024:1024 + n].view(dtype).view(shape)
+
+    def intact(raw, n):
+        r = raw.cpu().numpy()
+        return (r[:1024] == CAN).all() and (r[1024 + n:] == CAN).all()
+
+    outs = {}
+    for name, shape, dtype in [("cor", (S, M, 2), torch.int32), ("cnt", (S,), torch.int32),
+                               ("tr", (S, M, 2), torch.float32), ("st", (S, M), torch.uint8),
+                               ("H", (S, 9), torch.float64), ("ok", (S,), torch.int32),
+                               ("inl", (S, M), torch.uint8), ("itc", (S, kp.ransac_iters), torch.int32)]:
+        outs[name] = guarded(shape, dtype)
+    o = {n: v[1] for n, v in outs.items()}
+    k.corners(f[0], o["cor"], o["cnt"])
+    k.track(f[0], f[1], o["cor"], o["cnt"], o["tr"], o["st"])
+    # matches from the tracked points (host-side compaction, as the oracle's chain does)
+    torch.cuda.synchronize()
+    src = np.zeros((S, M, 2)); dst = np.zeros((S, M, 2)); mc = np.zeros(S, np.int32)
+    for s in range(S):
+        n = int(o["cnt"][s]); ok = o["st"][s, :n].cpu().numpy().astype(bool)
+        src[s, :ok.sum()] = o["tr"][s, :n].cpu().numpy()[ok]
+        dst[s, :ok.sum()] = o["cor"][s, :n].cpu().numpy()[ok] + 0.5
+        mc[s] = ok.sum()
+    k.ransac(torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda(), torch.from_numpy(mc).cuda(), o["H"],
+             o["inl"], o["itc"], o["ok"])
+    k.estimate(f[0], f[1], o["H"], o["ok"])
+    k.estimate_seq(f[1], f[2], o["H"], o["ok"])
+    k.estimate_seq(f[2], f[0], o["H"], o["ok"])
+    torch.cuda.synchronize()
+    for name, (raw, view) in outs.items():
+        assert intact(raw, view.numel() * view.element_size()), name
+    assert k.get_status() == 0
+    k.close()
