@@ -37,6 +37,7 @@ def test_warp_bitwise(cuda_lib, oracle_mod, W, H, S):
     cuda_lib.warp_frames(fin[..., :W], h, fout[..., :W])
     torch.cuda.synchronize()
     got = fout[..., :W].cpu().numpy()
+    assert np.all(fout[..., W:].cpu().numpy() == 3)                  # nothing written past the width
     want = oracle_mod.warp_frames(frames, Hs)
     assert np.array_equal(got, want), f"{(got != want).sum()} pixels differ"
     assert np.all(fout[..., W:].cpu().numpy() == 3)
@@ -161,6 +162,7 @@ def test_warp_fast_tiles(cuda_lib, oracle_mod, case):
     cuda_lib.warp_frames(fin[..., :W], torch.from_numpy(Hs).to(dev), fout[..., :W])
     torch.cuda.synchronize()
     got = fout[..., :W].cpu().numpy()
+    assert np.all(fout[..., W:].cpu().numpy() == 7)                  # nothing written past the width
     want = oracle_mod.warp_frames(frames, Hs)
     for s in range(S):
         assert np.array_equal(got[s], want[s]), f"{case} stream {s}: {(got[s] != want[s]).sum()} pixels differ"
